@@ -1,0 +1,392 @@
+"""Plain, slow, obviously correct Newton step on truncated power series.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Imports nothing from the
+product package.  Every function cites the passage of PAPER.md (P:line) it
+follows.  Scalars are field elements supporting + - * / and abs(): exact
+``fractions.Fraction`` (tier O-exact) or ``mpmath`` mpf in a private context
+of ``prec`` bits (tier O-hp).  Series are Python lists of d scalars
+(coefficient k = coefficient of t^k); the truncation drops t^{>=d}
+(reading R5).
+"""
+from __future__ import annotations
+
+from fractions import Fraction
+
+import mpmath
+import numpy as np
+
+
+# --------------------------------------------------------------------------
+# fields
+# --------------------------------------------------------------------------
+class ExactField:
+    """Exact rationals.  md limbs are dyadic, so conversion is exact."""
+    name = "exact"
+
+    def __init__(self):
+        self.zero = Fraction(0)
+        self.one = Fraction(1)
+
+    def num(self, f: float):
+        return Fraction(f)
+
+    def from_limbs(self, limbs):
+        s = Fraction(0)
+        for l in limbs:
+            s += Fraction(float(l))
+        return s
+
+    def to_fraction(self, v):
+        return v
+
+
+class MPField:
+    """mpmath at ``prec`` bits in a private context (no global state)."""
+
+    def __init__(self, prec: int):
+        self.ctx = mpmath.MPContext()
+        self.ctx.prec = prec
+        self.name = f"mp{prec}"
+        self.zero = self.ctx.mpf(0)
+        self.one = self.ctx.mpf(1)
+
+    def num(self, f: float):
+        return self.ctx.mpf(f)
+
+    def from_limbs(self, limbs):
+        # exact sum of dyadic limbs, rounded once to prec bits
+        return self.num_fraction(sum((Fraction(float(l)) for l in limbs), Fraction(0)))
+
+    def num_fraction(self, fr: Fraction):
+        return self.ctx.mpf(fr.numerator) / self.ctx.mpf(fr.denominator)
+
+    def to_fraction(self, v):
+        sign, man, e, _bc = self.ctx.mpf(v)._mpf_   # value = (-1)^sign man 2^e
+        m = -int(man) if sign else int(man)
+        return Fraction(m * 2 ** e) if e >= 0 else Fraction(m, 2 ** (-e))
+
+
+def field_for(K: int, exact: bool = False):
+    """O-exact, or O-hp at >= 2x the md bits (256 / 512 / 1024 for 2d / 4d / 8d)."""
+    if exact:
+        return ExactField()
+    return MPField({2: 256, 4: 512, 8: 1024}[K])
+
+
+# --------------------------------------------------------------------------
+# series (Eq.(14))
+# --------------------------------------------------------------------------
+def conv(a, b, d, F):
+    """Truncated Cauchy product c_k = sum_{j=0}^{k} a_j b_{k-j}, k < d.
+
+    Eq.(14) with the coefficients of negative index equal to
+    zero; the paper's padded terms are zero products and are omitted
+    (reading R6: same result)."""
+    c = []
+    for k in range(d):
+        s = F.zero
+        for j in range(k + 1):
+            s = s + a[j] * b[k - j]
+        c.append(s)
+    return c
+
+
+def unit_series(d, F):
+    return [F.one] + [F.zero] * (d - 1)
+
+
+def product(series_list, d, F):
+    """prod of the series in list order, left to right; empty product = 1."""
+    p = unit_series(d, F)
+    for s in series_list:
+        p = conv(p, s, d, F)
+    return p
+
+
+# --------------------------------------------------------------------------
+# reading system inputs (synth.System duck type: n, D, d, K, eq_ptr, mono_ptr,
+# var_idx, coeff [K][M], rhs [K][n][d])
+# --------------------------------------------------------------------------
+def read_x(x_planes, F):
+    """x float64 [K][n][d] (limb planes) -> list of n series of field scalars."""
+    K, n, d = x_planes.shape
+    return [[F.from_limbs(x_planes[:, j, k]) for k in range(d)] for j in range(n)]
+
+
+def read_coeffs(sys, F):
+    return [F.from_limbs(sys.coeff[:, t]) for t in range(sys.M)]
+
+
+def read_rhs(sys, F):
+    K, n, d = sys.rhs.shape
+    return [[F.from_limbs(sys.rhs[:, i, k]) for k in range(d)] for i in range(n)]
+
+
+def monomial_vars(sys, t):
+    return [int(v) for v in sys.var_idx[sys.mono_ptr[t]:sys.mono_ptr[t + 1]]]
+
+
+def eq_monomials(sys, i):
+    return range(int(sys.eq_ptr[i]), int(sys.eq_ptr[i + 1]))
+
+
+def jacobian_pattern(sys):
+    """Row i: sorted union of the variables of equation i's monomials (the
+    structural nonzeros of A_k, k = 0..D; Eq.(8))."""
+    rows = []
+    for i in range(sys.n):
+        s = set()
+        for t in eq_monomials(sys, i):
+            s.update(monomial_vars(sys, t))
+        rows.append(sorted(s))
+    return rows
+
+
+# --------------------------------------------------------------------------
+# evaluation and differentiation: the plain definition
+# --------------------------------------------------------------------------
+def monomial_value(x, vs, d, F):
+    """prod_{j in tau} x_j(t), truncated."""
+    return product([x[v] for v in vs], d, F)
+
+
+def monomial_partial(x, vs, j, d, F):
+    """d/dx_j prod_{l in tau} x_l = prod_{l in tau, l != j} x_l  (exponents 0/1,
+    reading R8); the empty product is the series 1 (m = 1, reading R7)."""
+    return product([x[v] for v in vs if v != j], d, F)
+
+
+def monomial_partials_split(x, vs, d, F):
+    """The same partials as ``monomial_partial``, each written as the product of
+    the variables before j times the product of the variables after j:
+    prod_{l != j} x_l = (prod_{l < j} x_l) * (prod_{l > j} x_l).  The two
+    factor lists are formed once (left to right, right to left).  Pinned
+    against ``monomial_partial`` in tests/test_oracle.py; used only to keep
+    the oracle affordable on large rows."""
+    m = len(vs)
+    before = [unit_series(d, F)]
+    for q in range(m - 1):
+        before.append(conv(before[-1], x[vs[q]], d, F))
+    after = [unit_series(d, F)]
+    for q in range(m - 1, 0, -1):
+        after.append(conv(after[-1], x[vs[q]], d, F))
+    after = after[::-1]  # after[q] = prod_{l > q} x_{v_l}
+    return [conv(before[q], after[q], d, F) for q in range(m)]
+
+
+def evaluate_row(sys, x, coeffs, rhs, i, d, F, split=False):
+    """Row i of (b, A): b_i(t) = r_i(t) - sum_tau c_tau x^tau(t) (reading R3,
+    P:317-319) and A[i][j](t) = sum_{tau ∋ j} c_tau d x^tau / d x_j, summed in
+    ascending monomial order (reading R20).  Returns (b_i series,
+    {j: series})."""
+    val = [F.zero] * d
+    row = {}
+    for t in eq_monomials(sys, i):
+        vs = monomial_vars(sys, t)
+        c = coeffs[t]
+        v = monomial_value(x, vs, d, F)
+        val = [val[k] + c * v[k] for k in range(d)]
+        if split:
+            parts = monomial_partials_split(x, vs, d, F)
+        else:
+            parts = [monomial_partial(x, vs, j, d, F) for j in vs]
+        for j, p in zip(vs, parts):
+            acc = row.get(j, [F.zero] * d)
+            row[j] = [acc[k] + c * p[k] for k in range(d)]
+    b = [rhs[i][k] - val[k] for k in range(d)]
+    return b, row
+
+
+def evaluate(sys, x, F, split=False, rows=None):
+    """All rows (or the listed ``rows``): returns (b, A) with b[i] a series and
+    A[i] a dict {j: series}.  x is a list of series (``read_x``)."""
+    d = sys.d
+    coeffs = read_coeffs(sys, F)
+    rhs = read_rhs(sys, F)
+    rows = range(sys.n) if rows is None else rows
+    b, A = {}, {}
+    for i in rows:
+        b[i], A[i] = evaluate_row(sys, x, coeffs, rhs, i, d, F, split)
+    return b, A
+
+
+# --------------------------------------------------------------------------
+# linear algebra
+# --------------------------------------------------------------------------
+def _abs(v):
+    return abs(v)
+
+
+def lu_factor(M, F):
+    """Gaussian elimination with partial pivoting, textbook (Doolittle).
+    Returns (LU, perm); raises ZeroDivisionError for a singular matrix."""
+    n = len(M)
+    a = [list(r) for r in M]
+    perm = list(range(n))
+    for c in range(n):
+        p = max(range(c, n), key=lambda r: _abs(a[r][c]))
+        if a[p][c] == 0:
+            raise ZeroDivisionError(f"singular A0 at column {c}")
+        if p != c:
+            a[c], a[p] = a[p], a[c]
+            perm[c], perm[p] = perm[p], perm[c]
+        piv = a[c][c]
+        for r in range(c + 1, n):
+            l = a[r][c] / piv
+            a[r][c] = l
+            if l != 0:
+                rc, rr = a[c], a[r]
+                for q in range(c + 1, n):
+                    rr[q] = rr[q] - l * rc[q]
+    return a, perm
+
+
+def lu_solve(LU, perm, rhs, F):
+    n = len(LU)
+    y = [rhs[perm[i]] for i in range(n)]
+    for i in range(n):
+        s = y[i]
+        for q in range(i):
+            s = s - LU[i][q] * y[q]
+        y[i] = s
+    for i in range(n - 1, -1, -1):
+        s = y[i]
+        for q in range(i + 1, n):
+            s = s - LU[i][q] * y[q]
+        y[i] = s / LU[i][i]
+    return y
+
+
+def dense_coeff(A, n, k, F):
+    """Dense n x n matrix A_k from the row dicts (off-pattern zeros)."""
+    M = [[F.zero] * n for _ in range(n)]
+    for i, row in A.items():
+        for j, s in row.items():
+            M[i][j] = s[k]
+    return M
+
+
+def matvec_sparse(A, k, v, n, F):
+    """(A_k v)_i over the structural entries of row i."""
+    out = [F.zero] * n
+    for i, row in A.items():
+        s = F.zero
+        for j, ser in row.items():
+            s = s + ser[k] * v[j]
+        out[i] = s
+    return out
+
+
+def solve(A, b, n, d, F, k_lo=0):
+    """Block forward substitution of Eq.(4):
+    for k = 0..d-1:  A_0 dx_k = b_k - sum_{j=1}^{k} A_j dx_{k-j}.
+    Returns dx as a list of d coefficient vectors (each a list of n)."""
+    LU, perm = lu_factor(dense_coeff(A, n, 0, F), F)
+    dx = []
+    for k in range(d):
+        rhs = [b[i][k] for i in range(n)]
+        for j in range(1, k + 1):
+            Av = matvec_sparse(A, j, dx[k - j], n, F)
+            rhs = [rhs[i] - Av[i] for i in range(n)]
+        dx.append(lu_solve(LU, perm, rhs, F))
+    return dx
+
+
+def residual(A, b, dx, n, d, F):
+    """r_k = b_k - sum_{j=0}^{k} A_j dx_{k-j}  ("report ||b(t) - A(t) dx(t)||")."""
+    r = []
+    for k in range(d):
+        rk = [b[i][k] for i in range(n)]
+        for j in range(0, k + 1):
+            Av = matvec_sparse(A, j, dx[k - j], n, F)
+            rk = [rk[i] - Av[i] for i in range(n)]
+        r.append(rk)
+    return r
+
+
+def series_norm(vecs):
+    """max over k of the vector 1-norm sum_i |v_k,i| (reading R16)."""
+    return max(sum(abs(v) for v in vk) for vk in vecs)
+
+
+def step(sys, x_planes, F, split=False):
+    """One Newton step (P:316-323 body, one iteration, all orders 0..D):
+    (A, b) := evaluate; dx := A \\ b; report ||b - A dx||; x := x + dx.
+    Returns a dict of field-valued results."""
+    n, d = sys.n, sys.d
+    x = read_x(x_planes, F)
+    b, A = evaluate(sys, x, F, split)
+    dx = solve(A, b, n, d, F)
+    r = residual(A, b, dx, n, d, F)
+    x_new = [[x[i][k] + dx[k][i] for k in range(d)] for i in range(n)]
+    bk = [[b[i][k] for i in range(n)] for k in range(d)]
+    return dict(x=x, b=b, A=A, dx=dx, r=r, x_new=x_new,
+                norm_b=series_norm(bk), norm_r=series_norm(r), norm_dx=series_norm(dx))
+
+
+# --------------------------------------------------------------------------
+# running-error scales -- float64 magnitudes only
+# --------------------------------------------------------------------------
+def _absconv(a, b, d):
+    c = np.zeros(d)
+    for k in range(d):
+        c[k] = np.dot(a[:k + 1], b[k::-1])
+    return c
+
+
+def scales(sys, x_planes):
+    """Magnitude scales for the tolerance rule ||gpu - oracle|| <= tol_p * s
+    (SURVEY.md 8(c) c.4), for the eval/diff outputs:
+
+    s_b[k,i]      = |r_i,k| + sum_tau |c_tau| (conv_{j in tau} |x_j|)_k
+    s_A[(i,j)][k] = sum_{tau ∋ j} |c_tau| (conv_{l in tau, l != j} |x_l|)_k
+
+    float64 magnitudes of the leading limbs (they scale errors; they are not
+    results)."""
+    n, d = sys.n, sys.d
+    xa = np.abs(x_planes[0])                      # [n][d]
+    ra = np.abs(sys.rhs[0])
+    ca = np.abs(sys.coeff[0])
+    s_b = np.zeros((d, n))
+    s_A = {}
+    for i in range(n):
+        acc = ra[i].copy()
+        for t in eq_monomials(sys, i):
+            vs = monomial_vars(sys, t)
+            p = np.zeros(d); p[0] = 1.0
+            for v in vs:
+                p = _absconv(p, xa[v], d)
+            acc += ca[t] * p
+            for j in vs:
+                q = np.zeros(d); q[0] = 1.0
+                for v in vs:
+                    if v != j:
+                        q = _absconv(q, xa[v], d)
+                s_A[(i, j)] = s_A.get((i, j), np.zeros(d)) + ca[t] * q
+        s_b[:, i] = acc
+    return dict(s_b=s_b, s_A=s_A)
+
+
+def stage_scales(sys, x_planes, A0_float, dx_float, s_b, s_A):
+    """Running-error scale of the stage solve:
+      m_k = s_b_k + sum_{j=1}^{k} (s_A_j |dx_{k-j}| + |A_j| e_{k-j}) + s_A_0 |dx_k|
+      e_k = |A_0^{-1}| m_k ;   s_k = max_i (e_k,i + |x_k,i| + |dx_k,i|)
+    |A_j| is bounded by s_A_j (the same sums of absolute products).  Inputs are
+    float64: A_0 [n][n] (for |A_0^{-1}|), dx [d][n]."""
+    n, d = sys.n, sys.d
+    SA = np.zeros((d, n, n))
+    for (i, j), ser in s_A.items():
+        SA[:, i, j] = ser
+    inv_abs = np.abs(np.linalg.inv(A0_float))
+    dxa = np.abs(dx_float)
+    xa = np.abs(x_planes[0]).T                     # [d][n]
+    e = np.zeros((d, n))
+    s = np.zeros(d)
+    for k in range(d):
+        m = s_b[k].copy()
+        for j in range(1, k + 1):
+            m += SA[j] @ dxa[k - j] + SA[j] @ e[k - j]
+        m += SA[0] @ dxa[k]
+        e[k] = inv_abs @ m
+        s[k] = np.max(e[k] + xa[k] + dxa[k])
+    return s, e

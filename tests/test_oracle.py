@@ -1,0 +1,345 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+-m "not gpu".  Each pin is chosen so that a plausible mistake in the oracle
+(a dropped term, a wrong index, a transposed operand, a sign) fails one of
+them.  None of these recompute the oracle's own formula.
+"""
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import sympy
+
+import synth
+from oracle import newton as O
+from oracle import paper
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+FX = O.ExactField()
+
+
+def _gold(name):
+    rows = []
+    with open(os.path.join(GOLD, name)) as f:
+        for line in f:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rows.append(line.split())
+    return rows
+
+
+# ---------------------------------------------------------------- paper values
+def test_T1_inverse_factorials_as_printed():
+    """T1: 1/k! printed to 2 digits; k=15 is the known garble (R27)."""
+    for k, inv, _prec, _eps in _gold("T1_tabMPneed.txt"):
+        k = int(k)
+        true = 1.0 / math.factorial(k)
+        printed = float(inv)
+        if k == 15:
+            assert abs(printed - true) / true < 0.015 and f"{true:.1e}" == "7.6e-13"
+        else:
+            assert f"{true:.1e}" == f"{printed:.1e}", (k, true, printed)
+
+
+def test_T1_eps_are_powers_of_two():
+    """T1 eps column = 2^-52, 2^-104, 2^-210, 2^-423, 2^-848."""
+    want = {"2.2e-16": 52, "4.9e-32": 104, "6.1e-64": 210, "4.6e-128": 423, "5.3e-256": 848}
+    for _k, _inv, _p, eps in _gold("T1_tabMPneed.txt"):
+        if eps != "-":
+            assert f"{2.0 ** -want[eps]:.1e}" == eps
+    assert synth.EPS_P == {2: 2.0 ** -104, 4: 2.0 ** -210, 8: 2.0 ** -423}
+
+
+def test_T1_precision_choice_vs_last_coefficient():
+    """T1's rationale: the last coefficient 1/k! must exceed the working eps."""
+    for k, _inv, prec, _eps in _gold("T1_tabMPneed.txt"):
+        k = int(k)
+        limbs = {"double": 1, "double_double": 2, "quad_double": 4, "octo_double": 8,
+                 "hexa_double": 16}[prec]
+        eps = {1: 2.0 ** -52, 2: 2.0 ** -104, 4: 2.0 ** -210, 8: 2.0 ** -423,
+               16: 2.0 ** -848}[limbs]
+        assert Fraction(1, math.factorial(k)) > Fraction(eps)
+
+
+def test_T2_totals_and_eq16_factors():
+    for limbs, a, s, m, tot in _gold("T2_tabcostmd.txt"):
+        limbs, a, s, m, tot = map(int, (limbs, a, s, m, tot))
+        assert a + s + m == tot == paper.T2[limbs][3]
+    rows = _gold("eq16_factors.txt")
+    for kind, key, val in rows:
+        if kind == "factor":
+            assert paper.T2[int(key)][3] / int(key) == float(val) == paper.INTENSITY_FACTORS[int(key)]
+    assert round(84 / 11.5, 2) == 7.30 and round(217.75 / 84, 2) == 2.59
+
+
+def test_eq12_job_list_and_count():
+    """Eq.(12)/(13): m=4 gives exactly the printed 7 products."""
+    fwd, bwd, cross = paper.reverse_mode_jobs(4)
+    assert fwd == [("x1", "x2"), ("f1", "x3"), ("f2", "x4")]
+    assert bwd == [("x4", "x3"), ("g1", "x2")]
+    assert sorted(cross) == [(2, "x1", "g1"), (3, "f1", "x4")]
+    assert len(_gold("eq12_m4_jobs.txt")) == 7
+    for m in range(3, 40):
+        f, b, c = paper.reverse_mode_jobs(m)
+        assert len(f) + len(b) + len(c) == paper.products_per_monomial(m) == 3 * m - 5
+    assert paper.products_per_monomial(1) == 0 and paper.products_per_monomial(2) == 1
+
+
+def test_count_laws():
+    """padded d^2 (S:201 d=5 -> 25) vs the triangular d(d+1)/2."""
+    assert paper.padded_products(5) == 25
+    for d in range(1, 70):
+        a = [Fraction(1)] * d
+        cnt = sum(k + 1 for k in range(d))
+        assert paper.triangular_products(d) == cnt
+    # SURVEY 8 closed form S(n) = 1.5n^2 - 3.5n + 2 for the one-column system
+    for n in range(3, 50):
+        S = sum(paper.products_per_monomial(m) for m in range(1, n + 1))
+        assert 2 * S == 3 * n * n - 7 * n + 4
+
+
+# ---------------------------------------------------------------- convolution
+def test_conv_spec_examples():
+    one_pt = [FX.one, FX.one, FX.zero]
+    assert O.conv(one_pt, one_pt, 3, FX) == [1, 2, 1]
+    e = [Fraction(1, math.factorial(k)) for k in range(4)]
+    assert O.conv(e, e, 4, FX) == [1, 2, 2, Fraction(4, 3)]
+
+
+def test_conv_exp_law_exact():
+    """exp(at) exp(bt) = exp((a+b)t): coefficients (a+b)^k/k! exactly (binomial theorem)."""
+    rng = np.random.default_rng(3)
+    for _ in range(5):
+        a, b = (Fraction(float(v)) for v in rng.uniform(-1, 1, 2))
+        d = 12
+        ea = [a ** k / math.factorial(k) for k in range(d)]
+        eb = [b ** k / math.factorial(k) for k in range(d)]
+        c = O.conv(ea, eb, d, FX)
+        assert c == [(a + b) ** k / math.factorial(k) for k in range(d)]
+        # operand order and a transposed index would break the law for a != b
+        assert O.conv(eb, ea, d, FX) == c
+
+
+def test_conv_binomial_law_exact():
+    """(1-t)^-a (1-t)^-b = (1-t)^-(a+b): coefficients C(k+a+b-1, k)."""
+    d = 15
+    for a in range(1, 5):
+        for b in range(1, 5):
+            sa = [Fraction(math.comb(k + a - 1, k)) for k in range(d)]
+            sb = [Fraction(math.comb(k + b - 1, k)) for k in range(d)]
+            assert O.conv(sa, sb, d, FX) == [math.comb(k + a + b - 1, k) for k in range(d)]
+
+
+# ---------------------------------------------------------------- eval / diff
+def _exp_x(alphas, d):
+    return [[Fraction(a) ** k / math.factorial(k) for k in range(d)] for a in alphas]
+
+
+def test_monomial_value_and_partials_closed_form():
+    """At x_j = exp(a_j t): value = exp(S t), d/dx_j = exp((S - a_j) t) (SURVEY c.5)."""
+    rng = np.random.default_rng(5)
+    alphas = [float(v) for v in rng.uniform(-1, 1, 6)]
+    d = 8
+    x = _exp_x(alphas, d)
+    vs = [0, 2, 3, 5]
+    S = sum(Fraction(alphas[v]) for v in vs)
+    assert O.monomial_value(x, vs, d, FX) == [S ** k / math.factorial(k) for k in range(d)]
+    for j in vs:
+        Sj = S - Fraction(alphas[j])
+        assert O.monomial_partial(x, vs, j, d, FX) == [Sj ** k / math.factorial(k) for k in range(d)]
+    split = O.monomial_partials_split(x, vs, d, FX)
+    assert split == [O.monomial_partial(x, vs, j, d, FX) for j in vs]
+
+
+def test_partials_split_equals_definition_random():
+    rng = np.random.default_rng(11)
+    d = 6
+    x = [[Fraction(float(v)) for v in rng.uniform(-2, 2, d)] for _ in range(7)]
+    for vs in ([3], [1, 4], [0, 1, 2], [0, 2, 3, 5, 6], list(range(7))):
+        assert O.monomial_partials_split(x, vs, d, FX) == \
+            [O.monomial_partial(x, vs, j, d, FX) for j in vs]
+    assert O.monomial_partial(x, [3], 3, d, FX) == O.unit_series(d, FX)  # m = 1 (R7)
+
+
+def test_inv1mt_binomials_and_zero_residual():
+    """x_j = 1/(1-t): monomial of m vars has coefficients C(k+m-1, m-1), partials
+    C(k+m-2, m-2); b = 0 exactly at the exact solution (SURVEY c.5)."""
+    sys_ = synth.inv1mt_system(8, 8, 2)
+    x = synth.make_x(sys_, "exact")
+    xs = O.read_x(x, FX)
+    b, A = O.evaluate(sys_, xs, FX)
+    for i in range(8):
+        assert all(v == 0 for v in b[i])
+        m = i + 1
+        for j, ser in A[i].items():
+            assert ser == [math.comb(k + m - 2, m - 2) if m >= 2 else (1 if k == 0 else 0)
+                           for k in range(sys_.d)]
+    assert max(math.comb(8 + 8 - 1, 7), 6435) == 6435  # C1 maximum (< 2^53)
+
+
+def test_spec_A0_row_at_exact_solution():
+    """n=3 lower-ones system at the exact solution: A0[2][j] = 1."""
+    sys_ = synth.triangular_system(3, 3, 2, seed=1)
+    xs = O.read_x(synth.make_x(sys_, "exact"), FX)
+    b, A = O.evaluate(sys_, xs, FX)
+    assert [A[2][j][0] for j in range(3)] == [1, 1, 1]
+
+
+def test_two_column_equals_sum_of_columns():
+    """Linearity: evaluating c1 x^E1 + c2 x^E2 = sum of the columns evaluated separately."""
+    sys2 = synth.banded_two_column_system(6, 3, 4, 2, seed=3)
+    xs = O.read_x(synth.make_x(sys2, "near", seed=4), FX)
+    b, A = O.evaluate(sys2, xs, FX)
+    rhs = O.read_rhs(sys2, FX)
+    co = O.read_coeffs(sys2, FX)
+    for i in range(6):
+        tot = [FX.zero] * sys2.d
+        for t in O.eq_monomials(sys2, i):
+            v = O.monomial_value(xs, O.monomial_vars(sys2, t), sys2.d, FX)
+            tot = [tot[k] + co[t] * v[k] for k in range(sys2.d)]
+        assert b[i] == [rhs[i][k] - tot[k] for k in range(sys2.d)]
+
+
+# ---------------------------------------------------------------- solve
+def _dense_block(A, b, n, d):
+    """Assemble Eq.(4) explicitly as an (nd) x (nd) sympy matrix."""
+    M = sympy.zeros(n * d, n * d)
+    rhs = sympy.zeros(n * d, 1)
+    for k in range(d):
+        for kk in range(k + 1):
+            j = k - kk
+            for i, row in A.items():
+                for c, ser in row.items():
+                    M[k * n + i, kk * n + c] = sympy.Rational(ser[j].numerator, ser[j].denominator)
+        for i in range(n):
+            rhs[k * n + i] = sympy.Rational(b[i][k].numerator, b[i][k].denominator)
+    return M, rhs
+
+
+def test_toeplitz_solve_vs_dense_block_system():
+    """n=3, d=4 block forward substitution = dense 12x12 solve (sympy, exact)."""
+    sys_ = synth.triangular_system(3, 3, 2, seed=7)
+    xs = O.read_x(synth.make_x(sys_, "near", seed=8), FX)
+    b, A = O.evaluate(sys_, xs, FX)
+    dx = O.solve(A, b, 3, 4, FX)
+    M, rhs = _dense_block(A, b, 3, 4)
+    sol = M.LUsolve(rhs)
+    for k in range(4):
+        for i in range(3):
+            assert Fraction(str(sol[k * 3 + i])) == dx[k][i]
+    r = O.residual(A, b, dx, 3, 4, FX)
+    assert all(v == 0 for rk in r for v in rk)
+
+
+def test_toeplitz_solve_vs_numpy_two_column():
+    sys_ = synth.banded_two_column_system(7, 3, 5, 2, seed=9)
+    xs = O.read_x(synth.make_x(sys_, "near", seed=2), FX)
+    b, A = O.evaluate(sys_, xs, FX)
+    n, d = 7, 6
+    dx = O.solve(A, b, n, d, FX)
+    M, rhs = _dense_block(A, b, n, d)
+    sol = np.linalg.solve(np.array(M.tolist(), dtype=float), np.array(rhs.tolist(), dtype=float))
+    got = np.array([float(dx[k][i]) for k in range(d) for i in range(n)])
+    assert np.allclose(got, sol[:, 0], rtol=1e-9, atol=1e-12)
+
+
+def test_zero_rhs_gives_zero_update():
+    """Eq.(11): QR dx_k = b_k = 0 => dx_k = 0."""
+    sys_ = synth.triangular_system(4, 5, 2, seed=1)
+    xs = O.read_x(synth.make_x(sys_, "near", seed=1), FX)
+    _, A = O.evaluate(sys_, xs, FX)
+    zero = {i: [FX.zero] * 6 for i in range(4)}
+    dx = O.solve(A, zero, 4, 6, FX)
+    assert all(v == 0 for dk in dx for v in dk)
+
+
+def test_lower_ones_textbook_solve():
+    """At x_j(0) = 1, A_0 of the triangular system is the lower-ones matrix L and
+    (L^-1 b)_i = b_i - b_{i-1} (SURVEY c.5)."""
+    sys_ = synth.triangular_system(6, 0, 2, seed=4)
+    x = np.zeros((2, 6, 1)); x[0, :, 0] = 1.0
+    xs = O.read_x(x, FX)
+    b, A = O.evaluate(sys_, xs, FX)
+    for i in range(6):
+        for j in range(6):
+            assert A[i].get(j, [0])[0] == (1 if j <= i else 0)
+    dx = O.solve(A, b, 6, 1, FX)
+    for i in range(6):
+        assert dx[0][i] == b[i][0] - (b[i - 1][0] if i else 0)
+
+
+# ---------------------------------------------------------------- Newton
+def test_quadratic_convergence_and_fixed_point():
+    """From 'start' (x_0 correct to half precision), iterated oracle
+    steps converge to the closed form; coefficient k is exact to ~delta^(2^i - k)
+    after i steps (SURVEY c.3).  At the exact solution the update is ~0."""
+    F = O.MPField(600)
+    n, D = 4, 7
+    sys_ = synth.triangular_system(n, D, 8, seed=21)  # 8 limbs: rhs accurate to 2^-424
+    exact = synth.make_x(sys_, "exact")
+    ex = O.read_x(exact, F)
+    x = synth.make_x(sys_, "start", seed=5).copy()
+    # the oracle iterates on field values; keep x as field series
+    xs = O.read_x(x, F)
+    errs = []
+    for it in range(1, 5):
+        b, A = O.evaluate(sys_, xs, F)
+        dx = O.solve(A, b, n, sys_.d, F)
+        xs = [[xs[j][k] + dx[k][j] for k in range(sys_.d)] for j in range(n)]
+        e = [max(abs(xs[j][k] - ex[j][k]) for j in range(n)) for k in range(sys_.d)]
+        errs.append(e)
+        good = 2 ** it - 2
+        for k in range(min(good + 1, sys_.d)):
+            assert e[k] < F.num(2.0 ** -380), (it, k, e[k])
+    assert errs[-1][-1] < F.num(2.0 ** -380)
+    # fixed point
+    b, A = O.evaluate(sys_, ex, F)
+    dx = O.solve(A, b, n, sys_.d, F)
+    assert max(abs(v) for dk in dx for v in dk) < F.num(2.0 ** -400)
+
+
+def test_step_norms_and_residual_exact():
+    sys_ = synth.build_config("C1")
+    x = synth.make_x(sys_, "near", seed=1)
+    out = O.step(sys_, x, FX)
+    assert out["norm_r"] == 0
+    assert out["norm_b"] == max(sum(abs(out["b"][i][k]) for i in range(8)) for k in range(9))
+    assert out["norm_dx"] > 0
+
+
+def test_mp_tier_matches_exact_tier():
+    sys_ = synth.triangular_system(5, 6, 4, seed=2)
+    x = synth.make_x(sys_, "near", seed=3)
+    ex = O.step(sys_, x, FX)
+    F = O.field_for(4)
+    hp = O.step(sys_, x, F)
+    for k in range(7):
+        for i in range(5):
+            assert abs(F.to_fraction(hp["dx"][k][i]) - ex["dx"][k][i]) <= \
+                Fraction(2) ** -480 * (1 + abs(ex["dx"][k][i]))
+
+
+# ---------------------------------------------------------------- generator sanity
+def test_rational_to_md_exact_and_nonoverlapping():
+    rng = np.random.default_rng(0)
+    for K in (2, 4, 8):
+        for _ in range(50):
+            num = int(rng.integers(1, 2 ** 62)) * 3 ** 40
+            den = 7 ** 50
+            limbs = synth.rational_to_md(num, den, K)
+            rem = Fraction(num, den) - sum(Fraction(l) for l in limbs)
+            assert abs(rem) <= abs(Fraction(limbs[-1])) * Fraction(2) ** -52
+            for a, b in zip(limbs, limbs[1:]):
+                assert b == 0 or abs(b) <= abs(a) * 2.0 ** -52
+
+
+def test_exact_x_is_rounded_closed_form():
+    sys_ = synth.triangular_system(3, 9, 4, seed=12)
+    x = synth.make_x(sys_, "exact")
+    a = Fraction(sys_.exact[1][1])
+    for k in range(10):
+        v = sum(Fraction(l) for l in x[:, 1, k])
+        want = a ** k / math.factorial(k)
+        assert abs(v - want) <= abs(want) * Fraction(2) ** -210
