@@ -1,0 +1,145 @@
+/* ns.h -- C ABI of libnewtonmd.so: one Newton step on truncated power series
+ * in double-double / quad-double / octo-double arithmetic on B200 (sm_100a).
+ *
+ * Method: arxiv 2301.12659 (J. Verschelde), PAPER.md.  One call performs one
+ * iteration of the Newton pseudo-code over all series orders
+ * 0..D:
+ *   (A(t), b(t)) := evaluate and differentiate f at x(t)
+ *   dx(t) := A(t) \ b(t)  -- Householder QR of A_0 once, then for
+ *            k = 0..D: b'_k = b_k - sum_{j>=1} A_j dx_{k-j},
+ *            y = Q^T b'_k, back substitution R dx_k = y
+ *   report ||b(t) - A(t) dx(t)||
+ *   x(t) := x(t) + dx(t)
+ *
+ * Conventions:
+ *  - precision = K = number of limbs: 2 (2d), 4 (4d), 8 (8d).  An md number is
+ *    an unevaluated sum of K nonoverlapping doubles, most significant first
+ *    (P:135-136).  Arrays of md numbers are stored as K LIMB PLANES (structure
+ *    of arrays): limb l of element e is at base[l * plane + e].
+ *  - dim n, degree D, d = D + 1 coefficients (reading R1: degree 31 = 32
+ *    coefficients).
+ *  - Layouts:  x, rhs   [K][n][d]     (variable-major series)
+ *              b, dx    [K][d][n]     (coefficient-major vectors)
+ *              A        [K][d][nnz]   (structural Jacobian, row CSR pattern)
+ *              A0       [K][n][n]     (dense leading block, row-major)
+ *              residual [K][3]        (||b||, ||b - A dx||, ||dx||: max over
+ *                                      k of the vector 1-norm, reading R16)
+ *  - Ownership: the caller owns every pointer it passes; device pointers must
+ *    be device memory of the handle's device.  The library owns all workspace
+ *    (allocated in ns_system_create, freed in ns_system_destroy).  No call
+ *    allocates, and no step call synchronises the host; everything is ordered
+ *    on the given CUDA stream (cudaStream_t passed as void*; NULL = legacy).
+ *  - Errors: argument/shape errors are detected before any launch and
+ *    returned; device-side conditions (zero R_jj, non-finite norms) set a
+ *    status word read by ns_get_status.  Nothing is printed, nothing throws.
+ *  - Threading: one handle per stream; handles are independent.
+ */
+#ifndef NS_H_
+#define NS_H_
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NS_OK = 0,
+  NS_EINVAL = 1,     /* bad argument (NULL pointer, negative size, bad flag)          */
+  NS_EPREC = 2,      /* precision not in {2,4,8} or not the handle's precision          */
+  NS_EDIM = 3,       /* dim / degree / batch do not match the handle                    */
+  NS_EMONO = 4,      /* malformed monomial list (empty, unsorted, duplicate, >= dim)    */
+  NS_ESINGULAR = 5,  /* (status) an R_jj was exactly zero                  */
+  NS_ENONFINITE = 6, /* (status) a norm was not finite                                  */
+  NS_ENOMEM = 7,     /* device allocation failed at create                              */
+  NS_ECUDA = 8,      /* a CUDA runtime call failed                                      */
+  NS_ENCCL = 9,      /* reserved: NCCL failure                                          */
+  NS_ESTATE = 10     /* NS_REUSE_QR without a cached factorisation                      */
+} ns_status;
+
+/* step flags */
+#define NS_REUSE_QR 1u    /* skip the QR of A_0, reuse the cached factors     */
+#define NS_NO_RESIDUAL 2u /* skip the residual norm ("can be omitted")          */
+#define NS_LEDGER 4u      /* time the kernel classes with CUDA events (T4 classes)         */
+
+typedef struct ns_system ns_system; /* opaque; owns all device workspace */
+
+typedef struct {
+  int32_t dim;        /* n                                                        */
+  int32_t degree;     /* D (D+1 coefficients)                                     */
+  int32_t precision;  /* K in {2,4,8}                                             */
+  int32_t n_monomials;/* M                                                        */
+  int32_t max_batch;  /* >= 1; paths for ns_newton_series_step_batched            */
+  const int32_t* eq_ptr;   /* host [dim+1]: monomials of eq i = [eq_ptr[i], eq_ptr[i+1])  */
+  const int32_t* mono_ptr; /* host [M+1]: variables of monomial t = var_idx[mono_ptr[t]..] */
+  const int32_t* var_idx;  /* host: strictly increasing per monomial, < dim (exponent 1)  */
+  const double* coeff;     /* host [K][M] md coefficient c_t; NULL = all ones             */
+  const double* rhs;       /* host [K][dim][D+1] right-hand side series r_i(t)            */
+} ns_system_desc;
+
+typedef struct {
+  uint32_t status_bits;  /* 1 = zero R_jj seen, 2 = non-finite norm                   */
+  int32_t qr_cached;     /* 1 if a factorisation is cached for NS_REUSE_QR            */
+} ns_step_info;
+
+/* kernel classes of T4; updates, qhb and bs are fused into one
+ * persistent stage kernel and reported together as "stage" */
+typedef struct {
+  double ms_convolution; /* eval/diff                                   */
+  double ms_qr;          /* Householder QR + unpack + tile inversion     */
+  double ms_stage;       /* updates + Q^T b + back substitution           */
+  double ms_residual;    /* residuals + x update + norms                 */
+  int64_t steps;         /* ledger steps accumulated                     */
+  int64_t qr_count;      /* QR factorisations performed                  */
+} ns_ledger;
+
+/* Create a handle for one system on CUDA device cuda_device; validates the
+ * descriptor (NS_EMONO / NS_EPREC / NS_EINVAL), uploads it, sizes and
+ * allocates all workspace (NS_ENOMEM).  *out is NULL on failure. */
+ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_system** out);
+void ns_system_destroy(ns_system* sys);
+
+/* One Newton step (see top).  x_series: device [K][dim][degree+1], updated in
+ * place.  residual_out: device [K][3] or NULL.  precision/dim/degree must equal
+ * the handle's (NS_EPREC / NS_EDIM).  Asynchronous on stream. */
+ns_status ns_newton_series_step(ns_system* sys, int precision, int dim, int degree, double* x_series,
+                                double* residual_out, uint32_t flags, void* stream);
+
+/* Same step for `batch` independent paths of the same monomial structure
+ * (SURVEY 8(e) C5).  x_series: device [batch][K][dim][degree+1];
+ * rhs: device [batch][K][dim][degree+1] or NULL (= the handle's rhs for every
+ * path); residual_out: device [batch][K][3] or NULL.  batch <= max_batch. */
+ns_status ns_newton_series_step_batched(ns_system* sys, int precision, int dim, int degree, int batch,
+                                        double* x_series, const double* rhs, double* residual_out,
+                                        uint32_t flags, void* stream);
+
+/* Parity/debug entry points: the same kernels as the step. */
+/* eval/diff only: b [K][d][n], A [K][d][nnz], A0 [K][n][n], all device */
+ns_status ns_eval_diff(ns_system* sys, const double* x_series, double* b, double* A, double* A0,
+                       void* stream);
+/* the structural pattern (host arrays [dim+1] and [nnz]); nnz via ns_nnz */
+int32_t ns_nnz(const ns_system* sys);
+ns_status ns_jacobian_pattern(const ns_system* sys, int32_t* row_ptr, int32_t* col_idx);
+/* solve only: QR of A0, then the stage loop for the given b, A; dx [K][d][n] device */
+ns_status ns_toeplitz_solve(ns_system* sys, const double* b, const double* A, const double* A0,
+                            double* dx, void* stream);
+/* R's diagonal (alpha_j, device [K][n]) of the cached factorisation */
+ns_status ns_get_r_diag(ns_system* sys, double* rdiag, void* stream);
+/* md primitives on device planar arrays [K][n]: op 0 add, 1 mul, 2 fma c+a*b
+ * (c input/output), 3 div a/b, 4 sqrt a, 5 sub a-b (tests of row a0) */
+ns_status ns_md_op(int precision, int op, int n, const double* a, const double* b, double* c,
+                   void* stream);
+
+/* Synchronises the handle's last stream and returns the device status word. */
+ns_status ns_get_status(ns_system* sys, ns_step_info* host_out);
+/* Synchronises; per-class milliseconds accumulated over steps run with NS_LEDGER. */
+ns_status ns_get_ledger(ns_system* sys, ns_ledger* host_out);
+ns_status ns_reset_ledger(ns_system* sys);
+/* Kernels launched by the last step call (for the bench's gpu_launches). */
+int32_t ns_last_launch_count(const ns_system* sys);
+const char* ns_strerror(ns_status s);
+const char* ns_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NS_H_ */

@@ -1,0 +1,386 @@
+// api.cu -- the C ABI of libnewtonmd.so (include/ns.h): descriptor validation,
+// workspace, launch sequence of one Newton step.  No allocation and no host
+// synchronisation inside a step; everything is ordered on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <set>
+#include <vector>
+
+#include "../../include/ns.h"
+#include "system.h"
+
+#define CK NS_CK
+#define dalloc ns_dalloc
+
+namespace {
+
+int cost_of_eq(const ns_system* s, int i) {
+  long long c = 0;
+  for (int t = s->h_eq_ptr[i]; t < s->h_eq_ptr[i + 1]; ++t) {
+    const int m = s->h_mono_ptr[t + 1] - s->h_mono_ptr[t];
+    // critical path ~ (m-1) dependent products plus the cross batch
+    c += (m <= 1) ? 1 : (3 * m - 5 > 0 ? 3 * m - 5 : 1);
+  }
+  return (int)std::min<long long>(c, 1 << 30);
+}
+
+template <int K>
+ns_status step_impl(ns_system* s, double* x, double* res_out, uint32_t flags, cudaStream_t st) {
+  const bool ledger = (flags & NS_LEDGER) != 0;
+  s->last_launches = 0;
+  if (ledger) CK(cudaEventRecord(s->ev[0], st));
+  ns_status r = Impl<K>::evaldiff(s, x, st);
+  if (r) return r;
+  if (ledger) CK(cudaEventRecord(s->ev[1], st));
+  if (!(flags & NS_REUSE_QR)) {
+    r = Impl<K>::qr(s, st);
+    if (r) return r;
+  }
+  if (ledger) CK(cudaEventRecord(s->ev[2], st));
+  r = Impl<K>::stage(s, 0, st);
+  if (r) return r;
+  if (ledger) CK(cudaEventRecord(s->ev[3], st));
+  r = Impl<K>::residual(s, x, res_out, st);
+  if (r) return r;
+  if (ledger) {
+    CK(cudaEventRecord(s->ev[4], st));
+    s->ledger_pending = true;
+    if (!(flags & NS_REUSE_QR)) s->ledger.qr_count += 1;
+  }
+  s->last_stream = st;
+  return NS_OK;
+}
+
+ns_status collect_ledger(ns_system* s) {
+  if (!s->ledger_pending) return NS_OK;
+  CK(cudaEventSynchronize(s->ev[4]));
+  float ms[4];
+  for (int i = 0; i < 4; ++i) CK(cudaEventElapsedTime(&ms[i], s->ev[i], s->ev[i + 1]));
+  s->ledger.ms_convolution += ms[0];
+  s->ledger.ms_qr += ms[1];
+  s->ledger.ms_stage += ms[2];
+  s->ledger.ms_residual += ms[3];
+  s->ledger.steps += 1;
+  s->ledger_pending = false;
+  return NS_OK;
+}
+
+
+void free_all(ns_system* s) {
+  void* ptrs[] = {s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst, s->row_ptr, s->col_idx, s->job_order,
+                  s->coeff, s->rhs, s->b, s->A, s->A0, s->W, s->vhead, s->beta, s->rdiag, s->R, s->Qt,
+                  s->invR, s->bp, s->dx, s->y, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
+                  s->bar, s->status, s->bws};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& e : s->ev)
+    if (e) cudaEventDestroy(e);
+}
+
+}  // namespace
+
+
+extern "C" {
+
+const char* ns_strerror(ns_status s) {
+  switch (s) {
+    case NS_OK: return "ok";
+    case NS_EINVAL: return "invalid argument";
+    case NS_EPREC: return "precision not in {2,4,8} or not the handle's";
+    case NS_EDIM: return "dim/degree/batch mismatch";
+    case NS_EMONO: return "malformed monomial list";
+    case NS_ESINGULAR: return "zero diagonal entry in R";
+    case NS_ENONFINITE: return "non-finite norm";
+    case NS_ENOMEM: return "device allocation failed";
+    case NS_ECUDA: return "CUDA runtime error";
+    case NS_ENCCL: return "NCCL error";
+    case NS_ESTATE: return "no cached QR factorisation";
+  }
+  return "unknown status";
+}
+
+const char* ns_build_info(void) {
+  return "libnewtonmd sm_100a; md K in {2,4,8}; FP64 CUDA cores; arxiv 2301.12659 Newton step";
+}
+
+ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_system** out) {
+  if (!out) return NS_EINVAL;
+  *out = nullptr;
+  if (!desc || !desc->eq_ptr || !desc->mono_ptr || !desc->var_idx || !desc->rhs) return NS_EINVAL;
+  const int K = desc->precision;
+  if (K != 2 && K != 4 && K != 8) return NS_EPREC;
+  const int n = desc->dim, D = desc->degree, M = desc->n_monomials;
+  if (n < 1 || D < 0 || M < 1 || desc->max_batch < 0) return NS_EDIM;
+  if (desc->eq_ptr[0] != 0 || desc->eq_ptr[n] != M) return NS_EMONO;
+  for (int i = 0; i < n; ++i)
+    if (desc->eq_ptr[i + 1] < desc->eq_ptr[i]) return NS_EMONO;
+  if (desc->mono_ptr[0] != 0) return NS_EMONO;
+  int m_max = 1;
+  for (int t = 0; t < M; ++t) {
+    const int a = desc->mono_ptr[t], b = desc->mono_ptr[t + 1];
+    if (b <= a) return NS_EMONO;
+    m_max = std::max(m_max, b - a);
+    for (int q = a; q < b; ++q) {
+      if (desc->var_idx[q] < 0 || desc->var_idx[q] >= n) return NS_EMONO;
+      if (q > a && desc->var_idx[q] <= desc->var_idx[q - 1]) return NS_EMONO;
+    }
+  }
+  ns_system* s = new (std::nothrow) ns_system();
+  if (!s) return NS_ENOMEM;
+  s->dev = cuda_device;
+  s->n = n;
+  s->D = D;
+  s->d = D + 1;
+  s->K = K;
+  s->M = M;
+  s->m_max = m_max;
+  s->max_batch = std::max(1, desc->max_batch);
+  s->TB = 32;
+  s->T = (n + s->TB - 1) / s->TB;
+  const int L = desc->mono_ptr[M];
+  s->h_eq_ptr.assign(desc->eq_ptr, desc->eq_ptr + n + 1);
+  s->h_mono_ptr.assign(desc->mono_ptr, desc->mono_ptr + M + 1);
+  s->h_var_idx.assign(desc->var_idx, desc->var_idx + L);
+  // Jacobian pattern: row i = sorted union of the variables of eq i
+  s->h_row_ptr.assign(n + 1, 0);
+  s->h_mono_dst.assign(L, 0);
+  for (int i = 0; i < n; ++i) {
+    std::set<int> vs;
+    for (int t = s->h_eq_ptr[i]; t < s->h_eq_ptr[i + 1]; ++t)
+      for (int q = s->h_mono_ptr[t]; q < s->h_mono_ptr[t + 1]; ++q) vs.insert(s->h_var_idx[q]);
+    const int base = (int)s->h_col_idx.size();
+    s->h_row_ptr[i] = base;
+    std::vector<int> cols(vs.begin(), vs.end());
+    s->h_col_idx.insert(s->h_col_idx.end(), cols.begin(), cols.end());
+    for (int t = s->h_eq_ptr[i]; t < s->h_eq_ptr[i + 1]; ++t)
+      for (int q = s->h_mono_ptr[t]; q < s->h_mono_ptr[t + 1]; ++q)
+        s->h_mono_dst[q] = base + (int)(std::lower_bound(cols.begin(), cols.end(), s->h_var_idx[q]) - cols.begin());
+  }
+  s->h_row_ptr[n] = (int)s->h_col_idx.size();
+  s->nnz = s->h_row_ptr[n];
+  // LPT order: most expensive equations first
+  s->h_job_order.resize(n);
+  for (int i = 0; i < n; ++i) s->h_job_order[i] = i;
+  std::vector<int> cost(n);
+  for (int i = 0; i < n; ++i) cost[i] = cost_of_eq(s, i);
+  std::stable_sort(s->h_job_order.begin(), s->h_job_order.end(),
+                   [&](int a, int b) { return cost[a] > cost[b]; });
+
+  ns_status st = NS_OK;
+  auto fail = [&](ns_status e) {
+    free_all(s);
+    delete s;
+    return e;
+  };
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return fail(NS_ECUDA);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cuda_device) != cudaSuccess) return fail(NS_ECUDA);
+  s->sms = prop.multiProcessorCount;
+  const size_t d = s->d, nn = (size_t)n * n;
+  bool ok = true;
+  ok &= dalloc(&s->eq_ptr, n + 1) == cudaSuccess;
+  ok &= dalloc(&s->mono_ptr, M + 1) == cudaSuccess;
+  ok &= dalloc(&s->var_idx, L) == cudaSuccess;
+  ok &= dalloc(&s->mono_dst, L) == cudaSuccess;
+  ok &= dalloc(&s->row_ptr, n + 1) == cudaSuccess;
+  ok &= dalloc(&s->col_idx, s->nnz) == cudaSuccess;
+  ok &= dalloc(&s->job_order, n) == cudaSuccess;
+  ok &= dalloc(&s->coeff, (size_t)K * M) == cudaSuccess;
+  ok &= dalloc(&s->rhs, (size_t)K * n * d) == cudaSuccess;
+  ok &= dalloc(&s->b, (size_t)K * d * n) == cudaSuccess;
+  ok &= dalloc(&s->A, (size_t)K * d * s->nnz) == cudaSuccess;
+  ok &= dalloc(&s->A0, (size_t)K * nn) == cudaSuccess;
+  ok &= dalloc(&s->W, (size_t)K * 2 * nn) == cudaSuccess;
+  ok &= dalloc(&s->vhead, (size_t)K * n) == cudaSuccess;
+  ok &= dalloc(&s->beta, (size_t)K * n) == cudaSuccess;
+  ok &= dalloc(&s->rdiag, (size_t)K * n) == cudaSuccess;
+  ok &= dalloc(&s->R, (size_t)K * nn) == cudaSuccess;
+  ok &= dalloc(&s->Qt, (size_t)K * nn) == cudaSuccess;
+  ok &= dalloc(&s->invR, (size_t)K * s->T * s->TB * s->TB) == cudaSuccess;
+  ok &= dalloc(&s->bp, (size_t)K * d * n) == cudaSuccess;
+  ok &= dalloc(&s->dx, (size_t)K * d * n) == cudaSuccess;
+  ok &= dalloc(&s->y, (size_t)K * n) == cudaSuccess;
+  ok &= dalloc(&s->rbuf, (size_t)K * d * n) == cudaSuccess;
+  ok &= dalloc(&s->knorm, (size_t)3 * K * d) == cudaSuccess;
+  ok &= dalloc(&s->res_tmp, (size_t)K * 3) == cudaSuccess;
+  ok &= dalloc(&s->job_counter, 1) == cudaSuccess;
+  ok &= dalloc(&s->bar, 4) == cudaSuccess;
+  ok &= dalloc(&s->status, 1) == cudaSuccess;
+  if (!ok) return fail(NS_ENOMEM);
+  switch (K) {
+    case 2: st = Impl<2>::setup(s); break;
+    case 4: st = Impl<4>::setup(s); break;
+    default: st = Impl<8>::setup(s); break;
+  }
+  if (st) return fail(st);
+  if (dalloc(&s->ws, (size_t)s->grid_ed * 3 * s->m_max * K * d) != cudaSuccess) return fail(NS_ENOMEM);
+  // upload
+  std::vector<double> coeff((size_t)K * M, 0.0);
+  if (desc->coeff) std::memcpy(coeff.data(), desc->coeff, sizeof(double) * K * M);
+  else
+    for (int t = 0; t < M; ++t) coeff[t] = 1.0;
+  ok = true;
+  ok &= cudaMemcpy(s->eq_ptr, s->h_eq_ptr.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(s->mono_ptr, s->h_mono_ptr.data(), sizeof(int) * (M + 1), cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(s->var_idx, s->h_var_idx.data(), sizeof(int) * L, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(s->mono_dst, s->h_mono_dst.data(), sizeof(int) * L, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(s->row_ptr, s->h_row_ptr.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(s->col_idx, s->h_col_idx.data(), sizeof(int) * s->nnz, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(s->job_order, s->h_job_order.data(), sizeof(int) * n, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(s->coeff, coeff.data(), sizeof(double) * K * M, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(s->rhs, desc->rhs, sizeof(double) * K * n * d, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemset(s->status, 0, sizeof(unsigned)) == cudaSuccess;
+  ok &= cudaMemset(s->bar, 0, 4 * sizeof(unsigned)) == cudaSuccess;
+  for (auto& e : s->ev) ok &= cudaEventCreate(&e) == cudaSuccess;
+  if (!ok) return fail(NS_ECUDA);
+  *out = s;
+  return NS_OK;
+}
+
+void ns_system_destroy(ns_system* s) {
+  if (!s) return;
+  cudaSetDevice(s->dev);
+  cudaDeviceSynchronize();
+  free_all(s);
+  delete s;
+}
+
+ns_status ns_newton_series_step(ns_system* s, int precision, int dim, int degree, double* x,
+                                double* res_out, uint32_t flags, void* stream) {
+  if (!s || !x) return NS_EINVAL;
+  if (precision != s->K) return NS_EPREC;
+  if (dim != s->n || degree != s->D) return NS_EDIM;
+  if (flags & ~(NS_REUSE_QR | NS_NO_RESIDUAL | NS_LEDGER)) return NS_EINVAL;
+  if ((flags & NS_REUSE_QR) && !s->qr_cached) return NS_ESTATE;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (flags & NS_LEDGER) {
+    ns_status r = collect_ledger(s);
+    if (r) return r;
+  }
+  switch (s->K) {
+    case 2: return step_impl<2>(s, x, res_out, flags, st);
+    case 4: return step_impl<4>(s, x, res_out, flags, st);
+    default: return step_impl<8>(s, x, res_out, flags, st);
+  }
+}
+
+ns_status ns_newton_series_step_batched(ns_system* s, int precision, int dim, int degree, int batch,
+                                        double* x, const double* rhs, double* res, uint32_t flags,
+                                        void* stream) {
+  if (!s || !x) return NS_EINVAL;
+  if (precision != s->K) return NS_EPREC;
+  if (dim != s->n || degree != s->D || batch < 0 || batch > s->max_batch) return NS_EDIM;
+  if (flags & ~(NS_NO_RESIDUAL)) return NS_EINVAL;
+  if (batch == 0) return NS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (s->K) {
+    case 2: return Impl<2>::batched(s, batch, x, rhs, res, flags, st);
+    case 4: return Impl<4>::batched(s, batch, x, rhs, res, flags, st);
+    default: return Impl<8>::batched(s, batch, x, rhs, res, flags, st);
+  }
+}
+
+ns_status ns_eval_diff(ns_system* s, const double* x, double* b, double* A, double* A0, void* stream) {
+  if (!s || !x) return NS_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  ns_status r;
+  s->last_launches = 0;
+  switch (s->K) {
+    case 2: r = Impl<2>::evaldiff(s, x, st); break;
+    case 4: r = Impl<4>::evaldiff(s, x, st); break;
+    default: r = Impl<8>::evaldiff(s, x, st); break;
+  }
+  if (r) return r;
+  const size_t K = s->K, d = s->d, n = s->n;
+  if (b) CK(cudaMemcpyAsync(b, s->b, sizeof(double) * K * d * n, cudaMemcpyDeviceToDevice, st));
+  if (A) CK(cudaMemcpyAsync(A, s->A, sizeof(double) * K * d * s->nnz, cudaMemcpyDeviceToDevice, st));
+  if (A0) CK(cudaMemcpyAsync(A0, s->A0, sizeof(double) * K * n * n, cudaMemcpyDeviceToDevice, st));
+  s->last_stream = st;
+  return NS_OK;
+}
+
+int32_t ns_nnz(const ns_system* s) { return s ? s->nnz : -1; }
+
+ns_status ns_jacobian_pattern(const ns_system* s, int32_t* row_ptr, int32_t* col_idx) {
+  if (!s || !row_ptr || !col_idx) return NS_EINVAL;
+  std::memcpy(row_ptr, s->h_row_ptr.data(), sizeof(int) * (s->n + 1));
+  std::memcpy(col_idx, s->h_col_idx.data(), sizeof(int) * s->nnz);
+  return NS_OK;
+}
+
+ns_status ns_toeplitz_solve(ns_system* s, const double* b, const double* A, const double* A0, double* dx,
+                            void* stream) {
+  if (!s || !b || !A || !A0 || !dx) return NS_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t K = s->K, d = s->d, n = s->n;
+  CK(cudaMemcpyAsync(s->b, b, sizeof(double) * K * d * n, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(s->A, A, sizeof(double) * K * d * s->nnz, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(s->A0, A0, sizeof(double) * K * n * n, cudaMemcpyDeviceToDevice, st));
+  ns_status r;
+  s->last_launches = 0;
+  switch (s->K) {
+    case 2: r = Impl<2>::qr(s, st); if (!r) r = Impl<2>::stage(s, 0, st); break;
+    case 4: r = Impl<4>::qr(s, st); if (!r) r = Impl<4>::stage(s, 0, st); break;
+    default: r = Impl<8>::qr(s, st); if (!r) r = Impl<8>::stage(s, 0, st); break;
+  }
+  if (r) return r;
+  CK(cudaMemcpyAsync(dx, s->dx, sizeof(double) * K * d * n, cudaMemcpyDeviceToDevice, st));
+  s->last_stream = st;
+  return NS_OK;
+}
+
+ns_status ns_get_r_diag(ns_system* s, double* rdiag, void* stream) {
+  if (!s || !rdiag) return NS_EINVAL;
+  if (!s->qr_cached) return NS_ESTATE;
+  CK(cudaMemcpyAsync(rdiag, s->rdiag, sizeof(double) * s->K * s->n, cudaMemcpyDeviceToDevice,
+                     (cudaStream_t)stream));
+  return NS_OK;
+}
+
+ns_status ns_get_status(ns_system* s, ns_step_info* out) {
+  if (!s || !out) return NS_EINVAL;
+  CK(cudaSetDevice(s->dev));
+  CK(cudaDeviceSynchronize());
+  unsigned v = 0;
+  CK(cudaMemcpy(&v, s->status, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  out->status_bits = v;
+  out->qr_cached = s->qr_cached ? 1 : 0;
+  return NS_OK;
+}
+
+ns_status ns_get_ledger(ns_system* s, ns_ledger* out) {
+  if (!s || !out) return NS_EINVAL;
+  ns_status r = collect_ledger(s);
+  if (r) return r;
+  *out = s->ledger;
+  return NS_OK;
+}
+
+ns_status ns_reset_ledger(ns_system* s) {
+  if (!s) return NS_EINVAL;
+  ns_status r = collect_ledger(s);
+  if (r) return r;
+  s->ledger = ns_ledger{};
+  return NS_OK;
+}
+
+int32_t ns_last_launch_count(const ns_system* s) { return s ? s->last_launches : -1; }
+
+}  // extern "C"
+
+extern "C" ns_status ns_md_op(int precision, int op, int n, const double* a, const double* b, double* c,
+                              void* stream) {
+  if (n < 0 || op < 0 || op > 5 || !a || !c || (op != 4 && !b)) return NS_EINVAL;
+  if (n == 0) return NS_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (precision) {
+    case 2: return Impl<2>::md_op(op, n, a, b, c, st);
+    case 4: return Impl<4>::md_op(op, n, a, b, c, st);
+    case 8: return Impl<8>::md_op(op, n, a, b, c, st);
+    default: return NS_EPREC;
+  }
+}

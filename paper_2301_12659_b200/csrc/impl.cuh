@@ -1,0 +1,194 @@
+// impl.cuh -- per-precision launchers (instantiated once per K in kernels_k{2,4,8}.cu).
+#pragma once
+#include <algorithm>
+
+#include "batched.cuh"
+#include "evaldiff.cuh"
+#include "md.cuh"
+#include "solve.cuh"
+#include "system.h"
+
+using ns::DevSys;
+#define CK NS_CK
+#define dalloc ns_dalloc
+
+namespace {
+template <int K>
+ns_status launch_evaldiff(ns_system* s, const double* x, cudaStream_t st) {
+  CK(cudaMemsetAsync(s->job_counter, 0, sizeof(int), st));
+  DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
+            s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
+  ns::evaldiff_kernel<K><<<s->grid_ed, 256, s->ed_smem, st>>>(ds, x, s->b, s->A, s->A0, s->ws,
+                                                              s->job_counter);
+  s->last_launches += 1;
+  CK(cudaGetLastError());
+  return NS_OK;
+}
+
+template <int K>
+ns_status launch_qr(ns_system* s, cudaStream_t st) {
+  CK(cudaMemsetAsync(s->bar, 0, 2 * sizeof(unsigned), st));
+  int n = s->n;
+  const double* A0 = s->A0;
+  double *W = s->W, *vh = s->vhead, *be = s->beta, *rd = s->rdiag;
+  unsigned *bar = s->bar, *stt = s->status;
+  void* args[] = {&n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt};
+  CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_kernel<K>, dim3(s->grid_qr), dim3(128),
+                                 args, 0, st));
+  const long long tot = (long long)K * n * n;
+  const int blocks = (int)std::min<long long>((tot + 255) / 256, 4LL * s->sms);
+  ns::qr_unpack_kernel<K><<<blocks, 256, 0, st>>>(n, s->W, s->R, s->Qt);
+  ns::invert_tiles_kernel<K><<<s->T, 256, 0, st>>>(n, s->TB, s->R, s->invR);
+  s->last_launches += 3;
+  CK(cudaGetLastError());
+  s->qr_cached = true;
+  return NS_OK;
+}
+
+template <int K>
+ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
+  CK(cudaMemsetAsync(s->bar + 2, 0, 2 * sizeof(unsigned), st));
+  CK(cudaMemsetAsync(s->dx, 0, sizeof(double) * (size_t)K * s->d * s->n, st));
+  DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
+            s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
+  ns::StageArgs a{s->b, s->A, s->Qt, s->R, s->invR, s->bp, s->dx, s->y, s->TB, k_lo};
+  unsigned* bar = s->bar + 2;
+  void* args[] = {&ds, &a, &bar};
+  CK(cudaLaunchCooperativeKernel((const void*)ns::stage_kernel<K>, dim3(s->grid_st), dim3(128), args, 0, st));
+  s->last_launches += 1;
+  return NS_OK;
+}
+
+template <int K>
+ns_status launch_residual(ns_system* s, double* x, double* res_out, cudaStream_t st) {
+  ns::residual_kernel<K><<<s->d, 256, 0, st>>>(s->n, s->d, 0, s->b, s->bp, s->A0, s->dx, s->rbuf, s->knorm);
+  const long long tot = (long long)s->n * s->d;
+  const int blocks = (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, 2LL * s->sms));
+  ns::finalize_kernel<K><<<blocks, 256, 0, st>>>(s->n, s->d, x, s->dx, s->knorm,
+                                                 res_out ? res_out : s->res_tmp, s->status);
+  s->last_launches += 2;
+  CK(cudaGetLastError());
+  return NS_OK;
+}
+
+template <int K>
+ns_status setup_grids(ns_system* s) {
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::householder_qr_kernel<K>, 128, 0));
+  if (occ < 1) return NS_ECUDA;
+  s->grid_qr = s->sms;  // one CTA per SM: a cheaper barrier than occ * sms
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::stage_kernel<K>, 128, 0));
+  if (occ < 1) return NS_ECUDA;
+  s->grid_st = s->sms;
+  s->ed_smem = sizeof(double) * (size_t)K * s->d;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::evaldiff_kernel<K>, 256, s->ed_smem));
+  if (occ < 1) return NS_ECUDA;
+  s->grid_ed = std::min(s->n, occ * s->sms);
+  return NS_OK;
+}
+
+}  // namespace
+namespace {
+
+template <int K>
+ns_status batched_impl(ns_system* s, int batch, double* x, const double* rhs, double* res, uint32_t flags,
+                       cudaStream_t st) {
+  (void)flags;
+  const int n = s->n, d = s->d, TB = 32, T = (n + TB - 1) / TB;
+  const int threads = 256, NW = threads / 32;
+  ns::BLayout L{};
+  // arrays in order: W, invR, b, dx, y, vhead, beta, knorm
+  const size_t sz[8] = {(size_t)K * 2 * n * n, (size_t)K * T * TB * TB, (size_t)K * d * n, (size_t)K * d * n,
+                        (size_t)K * n, (size_t)K * n, (size_t)K * n, (size_t)3 * K * d};
+  size_t* offs[8] = {&L.off_W, &L.off_invR, &L.off_b, &L.off_dx, &L.off_y, &L.off_vh, &L.off_beta, &L.off_kn};
+  const size_t smem_cap = 200 * 1024 / sizeof(double);  // leave room for static smem
+  // greedy: smallest, hottest arrays first into shared memory
+  const int order[8] = {4, 5, 6, 7, 2, 3, 1, 0};
+  size_t sm = 0;
+  size_t g = (size_t)K * d * s->nnz + (size_t)NW * 3 * s->m_max * K * d;  // A + warp series
+  L.off_A_g = 0;
+  L.off_ser_g = (size_t)K * d * s->nnz;
+  L.in_smem = 0;
+  for (int q = 0; q < 8; ++q) {
+    const int a = order[q];
+    if (sm + sz[a] <= smem_cap) {
+      *offs[a] = sm;
+      sm += sz[a];
+      L.in_smem |= 1u << a;
+    } else {
+      *offs[a] = g;
+      g += sz[a];
+    }
+  }
+  L.smem_doubles = sm;
+  L.gws_doubles = g;
+  const size_t smem_bytes = sm * sizeof(double);
+  if (cudaFuncSetAttribute(ns::batched_step_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem_bytes) != cudaSuccess)
+    return NS_ECUDA;
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::batched_step_kernel<K>, threads, smem_bytes));
+  if (occ < 1) return NS_ECUDA;
+  const int grid = std::min(batch, occ * s->sms);
+  const size_t need = (size_t)grid * g;
+  if (need > s->bws_per_path) {  // bws_per_path holds the allocated size in doubles
+    if (s->bws) cudaFree(s->bws);
+    s->bws = nullptr;
+    s->bws_per_path = 0;
+    if (dalloc(&s->bws, need) != cudaSuccess) return NS_ENOMEM;
+    s->bws_per_path = need;
+  }
+  DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
+            s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
+  ns::batched_step_kernel<K><<<grid, threads, smem_bytes, st>>>(ds, batch, x, rhs, res, s->bws, L, TB);
+  s->last_launches = 1;
+  s->last_stream = st;
+  CK(cudaGetLastError());
+  return NS_OK;
+}
+
+}  // namespace
+
+namespace {
+template <int K>
+__global__ void md_op_kernel(int op, int n, const double* a, const double* b, double* c) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    md::mdv<K> x = md::load<K>(a, n, i);
+    md::mdv<K> y = (op == 4) ? md::zero<K>() : md::load<K>(b, n, i);
+    md::mdv<K> r;
+    switch (op) {
+      case 0: r = md::add<K>(x, y); break;
+      case 1: r = md::mul<K>(x, y); break;
+      case 2: r = md::fma_acc<K>(md::load<K>(c, n, i), x, y); break;
+      case 3: r = md::div<K>(x, y); break;
+      case 4: r = md::sqrt<K>(x); break;
+      default: r = md::sub<K>(x, y); break;
+    }
+    md::store<K>(c, n, i, r);
+  }
+}
+}  // namespace
+
+template <int K>
+ns_status Impl<K>::setup(ns_system* s) { return setup_grids<K>(s); }
+template <int K>
+ns_status Impl<K>::evaldiff(ns_system* s, const double* x, cudaStream_t st) { return launch_evaldiff<K>(s, x, st); }
+template <int K>
+ns_status Impl<K>::qr(ns_system* s, cudaStream_t st) { return launch_qr<K>(s, st); }
+template <int K>
+ns_status Impl<K>::stage(ns_system* s, int k_lo, cudaStream_t st) { return launch_stage<K>(s, k_lo, st); }
+template <int K>
+ns_status Impl<K>::residual(ns_system* s, double* x, double* r, cudaStream_t st) {
+  return launch_residual<K>(s, x, r, st);
+}
+template <int K>
+ns_status Impl<K>::batched(ns_system* s, int batch, double* x, const double* rhs, double* res, uint32_t flags,
+                           cudaStream_t st) {
+  return batched_impl<K>(s, batch, x, rhs, res, flags, st);
+}
+template <int K>
+ns_status Impl<K>::md_op(int op, int n, const double* a, const double* b, double* c, cudaStream_t st) {
+  const int blocks = std::min(1024, (n + 127) / 128);
+  md_op_kernel<K><<<blocks, 128, 0, st>>>(op, n, a, b, c);
+  return cudaGetLastError() == cudaSuccess ? NS_OK : NS_ECUDA;
+}

@@ -1,0 +1,354 @@
+// solve.cuh -- the linear-algebra half of the Newton step:
+//   householder_qr_kernel : Householder QR of A_0, applied to the
+//                           augmented [A_0 | I] so that one pass yields R and Q^T
+//   invert_tiles_kernel   : inverses of the diagonal tiles of R, once per QR
+//                           (tiled back substitution)
+//   stage_kernel          : for k = k_lo..D:
+//                             b'_k = b_k - sum_{j=1}^{k} A_j dx_{k-j}   (updates)
+//                             y    = Q^T b'_k                           (qhb)
+//                             R dx_k = y by tiles, last to first        (bs)
+//   residual_kernel       : r_k = b'_k - A_0 dx_k (= b_k - sum_{j<=k} A_j dx_{k-j},
+//                           reading R17) and the per-k 1-norms of r, b, dx
+//   finalize_kernel       : x += dx; ||b||, ||r||, ||dx|| = max_k (reading R16)
+// Cooperative kernels use a grid barrier; one warp owns one row or column so
+// every md reduction has a fixed order (deterministic).
+#pragma once
+#include "common.cuh"
+
+namespace ns {
+
+__device__ __forceinline__ int gwarp() { return (blockIdx.x * blockDim.x + threadIdx.x) >> 5; }
+__device__ __forceinline__ int nwarps() { return (gridDim.x * blockDim.x) >> 5; }
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// ------------------------------------------------------------------ QR
+// W: column-major work matrix, limb planes: W[(l*ncol + c)*n + r], ncol = 2n.
+template <int K, bool CG>
+MD_INL md::mdv<K> ld(const double* base, long long stride, long long i) {
+  return CG ? md::load_cg<K>(base, stride, i) : md::load<K>(base, stride, i);
+}
+template <int K, bool CG>
+MD_INL void st(double* base, long long stride, long long i, const md::mdv<K>& v) {
+  if (CG) md::store_cg<K>(base, stride, i, v);
+  else md::store<K>(base, stride, i, v);
+}
+
+template <int K, bool CG = true>
+__device__ void make_reflector(int n, int j, double* W, double* vhead, double* beta, double* rdiag,
+                               unsigned* status) {
+  const int ncol = 2 * n;
+  const long long ls = (long long)ncol * n;
+  const int lane = lane_id();
+  md::mdv<K> sig = md::zero<K>();
+  for (int r = j + lane; r < n; r += 32) {
+    md::mdv<K> v = ld<K, CG>(W, ls, (long long)j * n + r);
+    sig = md::fma_acc<K>(sig, v, v);
+  }
+  sig = md::group_sum<K>(sig, 32);
+  const md::mdv<K> x0 = ld<K, CG>(W, ls, (long long)j * n + j);
+  md::mdv<K> nrm = md::sqrt<K>(sig);
+  // alpha = -sign(x0) ||x||, sign(0) = +1 (reading R13)
+  md::mdv<K> alpha = md::is_negative<K>(x0) ? nrm : md::neg<K>(nrm);
+  md::mdv<K> v0 = md::sub<K>(x0, alpha);
+  md::mdv<K> bt = md::zero<K>();
+  if (!md::is_zero<K>(sig)) {
+    // v^T v = -2 alpha v0, beta = 2 / v^T v = -1 / (alpha v0)
+    bt = md::neg<K>(md::div<K>(md::from_double<K>(1.0), md::mul<K>(alpha, v0)));
+  } else if (lane == 0 && status) {
+    atomicOr(status, ST_SINGULAR);
+  }
+  if (lane == 0) {
+    st<K, CG>(vhead, n, j, v0);
+    st<K, CG>(beta, n, j, bt);
+    if (rdiag) st<K, CG>(rdiag, n, j, alpha);
+    st<K, CG>(W, ls, (long long)j * n + j, alpha);
+  }
+}
+
+// column c -= beta_j v (v^T column c), rows j..n-1
+template <int K, bool CG = true>
+__device__ void apply_reflector(int n, int j, int c, double* W, const double* vhead, const double* beta) {
+  const int ncol = 2 * n;
+  const long long ls = (long long)ncol * n;
+  const int lane = lane_id();
+  const md::mdv<K> v0 = ld<K, CG>(vhead, n, j);
+  md::mdv<K> dot = md::zero<K>();
+  for (int r = j + lane; r < n; r += 32) {
+    md::mdv<K> v = (r == j) ? v0 : ld<K, CG>(W, ls, (long long)j * n + r);
+    md::mdv<K> w = ld<K, CG>(W, ls, (long long)c * n + r);
+    dot = md::fma_acc<K>(dot, v, w);
+  }
+  dot = md::group_sum<K>(dot, 32);
+  const md::mdv<K> bt = ld<K, CG>(beta, n, j);
+  const md::mdv<K> nw = md::neg<K>(md::mul<K>(bt, dot));
+  for (int r = j + lane; r < n; r += 32) {
+    md::mdv<K> v = (r == j) ? v0 : ld<K, CG>(W, ls, (long long)j * n + r);
+    md::mdv<K> w = ld<K, CG>(W, ls, (long long)c * n + r);
+    w = md::fma_acc<K>(w, nw, v);
+    st<K, CG>(W, ls, (long long)c * n + r, w);
+  }
+}
+
+// One Householder step per grid barrier; the owner of column j+1 applies H_j to
+// it first and then forms reflector j+1 (look-ahead of one column).
+template <int K>
+__global__ void __launch_bounds__(128) householder_qr_kernel(int n, const double* __restrict__ A0,
+                                                             double* W, double* vhead, double* beta,
+                                                             double* rdiag, unsigned* bar,
+                                                             unsigned* status) {
+  const int ncol = 2 * n;
+  const long long ls = (long long)ncol * n;
+  const int gw = gwarp(), nw = nwarps();
+  // W = [A0 | I], column major
+  const long long tot = (long long)K * ncol * n;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(t % n);
+    const long long lc = t / n;
+    const int c = (int)(lc % ncol), l = (int)(lc / ncol);
+    double v;
+    if (c < n) v = A0[((long long)l * n + r) * n + c];
+    else v = (l == 0 && r == c - n) ? 1.0 : 0.0;
+    __stcg(W + (long long)l * ls + (long long)c * n + r, v);
+  }
+  grid_sync(bar);
+  if (gw == 0) make_reflector<K>(n, 0, W, vhead, beta, rdiag, status);
+  grid_sync(bar);
+  for (int j = 0; j < n; ++j) {
+    const int look = j + 1;
+    if (look < n && (look % nw) == gw) {
+      apply_reflector<K>(n, j, look, W, vhead, beta);
+      __syncwarp();
+      make_reflector<K>(n, look, W, vhead, beta, rdiag, status);
+    }
+    for (int c = gw; c < ncol; c += nw) {
+      if (c > j && c != look) apply_reflector<K>(n, j, c, W, vhead, beta);
+    }
+    grid_sync(bar);
+  }
+}
+
+// Row-major copies for the stage loop: R[r][c] (upper, diagonal = alpha) and
+// Qt[r][c] = (Q^T)[r][c].
+template <int K>
+__global__ void qr_unpack_kernel(int n, const double* __restrict__ W, double* R, double* Qt) {
+  const int ncol = 2 * n;
+  const long long ls = (long long)ncol * n;
+  const long long tot = (long long)K * n * n;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(t % n);
+    const long long lr = t / n;
+    const int r = (int)(lr % n), l = (int)(lr / n);
+    R[t] = (c >= r) ? W[l * ls + (long long)c * n + r] : 0.0;
+    Qt[t] = W[l * ls + (long long)(n + c) * n + r];
+  }
+}
+
+// inverse of the diagonal tile t of R (size nb <= 32): one warp per column of
+// the inverse; X[r][c] = -(sum_{q=r+1}^{c} R[r][q] X[q][c]) / R[r][r].
+// invR layout: [K][T][32][32] row-major per tile.
+template <int K>
+__global__ void __launch_bounds__(256) invert_tiles_kernel(int n, int TB, const double* __restrict__ R,
+                                                           double* invR) {
+  const int t = blockIdx.x;
+  const int t0 = t * TB;
+  const int nb = min(TB, n - t0);
+  const int lane = lane_id();
+  const int T = (n + TB - 1) / TB;
+  const long long lsR = (long long)n * n;
+  const long long lsI = (long long)T * TB * TB;
+  // 1 / R_qq for q = lane
+  md::mdv<K> inv_d = md::zero<K>();
+  if (lane < nb) {
+    md::mdv<K> rqq = md::load<K>(R, lsR, (long long)(t0 + lane) * n + t0 + lane);
+    inv_d = md::div<K>(md::from_double<K>(1.0), rqq);
+  }
+  for (int c = threadIdx.x >> 5; c < TB; c += blockDim.x >> 5) {  // column of the inverse
+    md::mdv<K> X = md::zero<K>();  // lane q holds X[q][c]
+    if (c < nb) {
+      if (lane == c) X = inv_d;
+      for (int r = c - 1; r >= 0; --r) {
+        md::mdv<K> p = md::zero<K>();
+        if (lane > r && lane <= c) {
+          md::mdv<K> rr = md::load<K>(R, lsR, (long long)(t0 + r) * n + t0 + lane);
+          p = md::mul<K>(rr, X);
+        }
+        p = md::group_sum<K>(p, 32);
+        md::mdv<K> idr = md::shfl<K>(inv_d, r);
+        md::mdv<K> xr = md::neg<K>(md::mul<K>(p, idr));
+        if (lane == r) X = xr;
+      }
+    }
+    // store column c of the tile inverse (zeros outside nb)
+    if (lane < TB) {
+      md::mdv<K> v = (lane < nb && c < nb && lane <= c) ? X : md::zero<K>();
+      md::store<K>(invR, lsI, (long long)t * TB * TB + (long long)lane * TB + c, v);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ stage loop
+struct StageArgs {
+  const double* b;     // [K][d][n]
+  const double* A;     // [K][d][nnz]
+  const double* Qt;    // [K][n][n] row-major
+  const double* R;     // [K][n][n] row-major upper
+  const double* invR;  // [K][T][TB][TB]
+  double* bp;          // [K][d][n]  b'_k
+  double* dx;          // [K][d][n]
+  double* y;           // [K][n]
+  int TB;
+  int k_lo;
+};
+
+template <int K>
+__global__ void __launch_bounds__(128) stage_kernel(DevSys s, StageArgs a, unsigned* bar) {
+  const int n = s.n, d = s.d, nnz = s.nnz;
+  const int gw = gwarp(), nw = nwarps(), lane = lane_id();
+  const long long lsV = (long long)d * n;     // limb stride of [K][d][n]
+  const long long lsA = (long long)d * nnz;
+  const long long lsM = (long long)n * n;
+  const int TB = a.TB;
+  const int T = (n + TB - 1) / TB;
+  const long long lsI = (long long)T * TB * TB;
+  for (int k = a.k_lo; k < d; ++k) {
+    // ---- updates: b'_k = b_k - sum_{j=1}^{k} A_j dx_{k-j}
+    for (int i = gw; i < n; i += nw) {
+      const int r0 = s.row_ptr[i], len = s.row_ptr[i + 1] - r0;
+      md::mdv<K> acc = md::zero<K>();
+      const int tot = (k - a.k_lo) * len;  // stages below k_lo are inactive (dx = 0)
+      for (int t = lane; t < tot; t += 32) {
+        const int j = 1 + t / len;
+        const int e = r0 + t % len;
+        md::mdv<K> aij = md::load<K>(a.A + (long long)j * nnz, lsA, e);
+        md::mdv<K> xv = md::load_cg<K>(a.dx + (long long)(k - j) * n, lsV, s.col_idx[e]);
+        acc = md::fma_acc<K>(acc, aij, xv);
+      }
+      acc = md::group_sum<K>(acc, 32);
+      if (lane == 0) {
+        md::mdv<K> bk = md::load<K>(a.b + (long long)k * n, lsV, i);
+        md::store_cg<K>(a.bp + (long long)k * n, lsV, i, md::sub<K>(bk, acc));
+      }
+    }
+    grid_sync(bar);
+    // ---- qhb: y = Q^T b'_k
+    for (int i = gw; i < n; i += nw) {
+      md::mdv<K> acc = md::zero<K>();
+      for (int c = lane; c < n; c += 32) {
+        md::mdv<K> q = md::load<K>(a.Qt, lsM, (long long)i * n + c);
+        md::mdv<K> v = md::load_cg<K>(a.bp + (long long)k * n, lsV, c);
+        acc = md::fma_acc<K>(acc, q, v);
+      }
+      acc = md::group_sum<K>(acc, 32);
+      if (lane == 0) md::store_cg<K>(a.y, n, i, acc);
+    }
+    grid_sync(bar);
+    // ---- bs: tiles last to first
+    for (int t = T - 1; t >= 0; --t) {
+      const int t0 = t * TB, t1 = min(n, t0 + TB);
+      // z_r = y_r - sum_{c >= t1} R[r][c] dx_k[c]   (z kept in y)
+      if (t < T - 1) {
+        for (int r = t0 + gw; r < t1; r += nw) {
+          md::mdv<K> acc = md::zero<K>();
+          for (int c = t1 + lane; c < n; c += 32) {
+            md::mdv<K> rv = md::load<K>(a.R, lsM, (long long)r * n + c);
+            md::mdv<K> xv = md::load_cg<K>(a.dx + (long long)k * n, lsV, c);
+            acc = md::fma_acc<K>(acc, rv, xv);
+          }
+          acc = md::group_sum<K>(acc, 32);
+          if (lane == 0) {
+            md::mdv<K> yr = md::load_cg<K>(a.y, n, r);
+            md::store_cg<K>(a.y, n, r, md::sub<K>(yr, acc));
+          }
+        }
+        grid_sync(bar);
+      }
+      // dx_k[r] = sum_{c in tile} invR_t[r][c] z_c
+      for (int r = t0 + gw; r < t1; r += nw) {
+        md::mdv<K> acc = md::zero<K>();
+        for (int c = t0 + lane; c < t1; c += 32) {
+          md::mdv<K> iv = md::load<K>(a.invR, lsI, (long long)t * TB * TB + (long long)(r - t0) * TB + (c - t0));
+          md::mdv<K> zv = md::load_cg<K>(a.y, n, c);
+          acc = md::fma_acc<K>(acc, iv, zv);
+        }
+        acc = md::group_sum<K>(acc, 32);
+        if (lane == 0) md::store_cg<K>(a.dx + (long long)k * n, lsV, r, acc);
+      }
+      grid_sync(bar);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ residual and norms
+// One CTA per coefficient k: r_k,i = b'_k,i - sum_c A0[i][c] dx_k[c];
+// knorm[k][0..2] = sum_i |b_k,i|, sum_i |r_k,i|, sum_i |dx_k,i|   (md, [3][K][d])
+template <int K>
+__global__ void __launch_bounds__(256) residual_kernel(int n, int d, int k_lo, const double* __restrict__ b,
+                                                       const double* __restrict__ bp,
+                                                       const double* __restrict__ A0,
+                                                       const double* __restrict__ dx, double* rbuf,
+                                                       double* knorm) {
+  const int k = blockIdx.x;
+  const int w = threadIdx.x >> 5, nwb = blockDim.x >> 5, lane = lane_id();
+  const long long lsV = (long long)d * n, lsM = (long long)n * n;
+  for (int i = w; i < n; i += nwb) {
+    md::mdv<K> acc = md::zero<K>();
+    if (k >= k_lo) {
+      for (int c = lane; c < n; c += 32) {
+        md::mdv<K> av = md::load<K>(A0, lsM, (long long)i * n + c);
+        md::mdv<K> xv = md::load<K>(dx + (long long)k * n, lsV, c);
+        acc = md::fma_acc<K>(acc, av, xv);
+      }
+      acc = md::group_sum<K>(acc, 32);
+    }
+    if (lane == 0) {
+      md::mdv<K> r = (k >= k_lo) ? md::sub<K>(md::load<K>(bp + (long long)k * n, lsV, i), acc)
+                                 : md::load<K>(b + (long long)k * n, lsV, i);
+      md::store<K>(rbuf + (long long)k * n, lsV, i, r);
+    }
+  }
+  __syncthreads();
+  // three 1-norms, one warp each, fixed order
+  if (w < 3) {
+    const double* src = (w == 0) ? b : ((w == 1) ? rbuf : dx);
+    md::mdv<K> acc = md::zero<K>();
+    for (int i = lane; i < n; i += 32) {
+      md::mdv<K> v = md::load<K>(src + (long long)k * n, lsV, i);
+      if (w == 2 && k < k_lo) v = md::zero<K>();
+      acc = md::add<K>(acc, md::absv<K>(v));
+    }
+    acc = md::group_sum<K>(acc, 32);
+    if (lane == 0) md::store<K>(knorm + (long long)w * K * d, d, k, acc);
+  }
+}
+
+// x += dx (one thread per coefficient); warp 0 of block 0 reduces the norms.
+template <int K>
+__global__ void finalize_kernel(int n, int d, double* x, const double* __restrict__ dx,
+                                const double* __restrict__ knorm, double* res_out, unsigned* status) {
+  const long long lsX = (long long)n * d, lsV = (long long)d * n;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)n * d;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(t / d), k = (int)(t % d);
+    md::mdv<K> xv = md::load<K>(x, lsX, t);
+    md::mdv<K> dv = md::load<K>(dx + (long long)k * n, lsV, j);
+    md::store<K>(x, lsX, t, md::add<K>(xv, dv));
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int w = 0; w < 3; ++w) {
+      md::mdv<K> best = md::zero<K>();
+      if (lane == 0) {
+        for (int k = 0; k < d; ++k) {
+          md::mdv<K> v = md::load<K>(knorm + (long long)w * K * d, d, k);
+          if (md::greater<K>(v, best)) best = v;
+        }
+        md::store<K>(res_out, 3, w, best);
+        if (!isfinite(best.x[0])) atomicOr(status, ST_NONFINITE);
+      }
+    }
+  }
+}
+
+}  // namespace ns

@@ -1,0 +1,64 @@
+// system.h -- the handle behind the opaque ns_system (include/ns.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "../../include/ns.h"
+
+struct ns_system {
+  int dev = 0;
+  int n = 0, D = 0, d = 0, K = 0, M = 0, nnz = 0, m_max = 0, max_batch = 1;
+  int TB = 32, T = 1;
+  int sms = 0;
+  // host copies
+  std::vector<int> h_eq_ptr, h_mono_ptr, h_var_idx, h_row_ptr, h_col_idx, h_mono_dst, h_job_order;
+  // device system
+  int *eq_ptr = nullptr, *mono_ptr = nullptr, *var_idx = nullptr, *mono_dst = nullptr;
+  int *row_ptr = nullptr, *col_idx = nullptr, *job_order = nullptr;
+  double *coeff = nullptr, *rhs = nullptr;
+  // workspace
+  double *b = nullptr, *A = nullptr, *A0 = nullptr, *W = nullptr, *vhead = nullptr, *beta = nullptr;
+  double *rdiag = nullptr, *R = nullptr, *Qt = nullptr, *invR = nullptr, *bp = nullptr, *dx = nullptr;
+  double *y = nullptr, *rbuf = nullptr, *knorm = nullptr, *res_tmp = nullptr, *ws = nullptr;
+  int* job_counter = nullptr;
+  unsigned* bar = nullptr;     // [4]: qr barrier, stage barrier
+  unsigned* status = nullptr;  // device status word
+  int grid_ed = 0, grid_qr = 0, grid_st = 0;
+  size_t ed_smem = 0;
+  bool qr_cached = false;
+  cudaStream_t last_stream = nullptr;
+  // ledger
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  bool ledger_pending = false;
+  ns_ledger ledger{};
+  int last_launches = 0;
+  // batched
+  double* bws = nullptr;
+  size_t bws_per_path = 0;
+  size_t batched_smem = 0;
+};
+
+
+// per-precision entry points, defined in kernels_k{2,4,8}.cu (impl.cuh)
+template <int K>
+struct Impl {
+  static ns_status setup(ns_system* s);
+  static ns_status evaldiff(ns_system* s, const double* x, cudaStream_t st);
+  static ns_status qr(ns_system* s, cudaStream_t st);
+  static ns_status stage(ns_system* s, int k_lo, cudaStream_t st);
+  static ns_status residual(ns_system* s, double* x, double* res_out, cudaStream_t st);
+  static ns_status batched(ns_system* s, int batch, double* x, const double* rhs, double* res,
+                           uint32_t flags, cudaStream_t st);
+  static ns_status md_op(int op, int n, const double* a, const double* b, double* c, cudaStream_t st);
+};
+
+#define NS_CK(x)                               \
+  do {                                         \
+    if ((x) != cudaSuccess) return NS_ECUDA;   \
+  } while (0)
+
+template <typename T>
+inline cudaError_t ns_dalloc(T** p, size_t count) {
+  return cudaMalloc((void**)p, (count > 0 ? count : 1) * sizeof(T));
+}

@@ -1,0 +1,298 @@
+"""GPU parity of the whole hot path against the oracle,
+through the C ABI, on seeded synthetic inputs (synth).
+
+Tolerance (north_star): |gpu - oracle| <= tol_p * s elementwise, tol_p = 1e-28
+(2d), 1e-60 (4d), 1e-120 (8d), s the running-error scale of SURVEY 8(c) c.4.
+The tests also report the error in units of eps_p (T1) and fail above 64 eps_p,
+which flags a bug long before the tolerance would.
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import newton as O
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not H.gpu_available():
+        pytest.skip("no CUDA device")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _handle(sys_, max_batch=1):
+    import paper_2301_12659_b200 as P
+    return P.NewtonSystem.from_system(sys_, max_batch=max_batch)
+
+
+def _np(t):
+    _torch().cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def _run_all(sys_, x_np):
+    """eval/diff, solve of the GPU's own (b, A, A0), and one full step."""
+    torch = _torch()
+    h = _handle(sys_)
+    x = torch.tensor(x_np, device="cuda:0")
+    b, A, A0 = h.eval_diff(x)
+    dx = h.toeplitz_solve(b, A, A0)
+    rdiag = h.r_diag()
+    x2 = x.clone()
+    res = torch.zeros((sys_.K, 3), dtype=torch.float64, device="cuda:0")
+    h.step(x2, res)
+    st = h.status()
+    return dict(h=h, b=_np(b), A=_np(A), A0=_np(A0), dx=_np(dx), x_new=_np(x2), res=_np(res),
+                rdiag=_np(rdiag), status=st.status_bits, pattern=h.pattern())
+
+
+def _full_parity(sys_, x_np, F, eps_cap=64.0):
+    g = _run_all(sys_, x_np)
+    out = H.step_oracle(sys_, x_np, F)
+    n, d, K = sys_.n, sys_.d, sys_.K
+    ed = H.eval_diff_errors(sys_, x_np, g["b"], g["A"], list(range(n)), F, g["pattern"])
+    assert ed["b"] <= 1 and ed["A"] <= 1, ed
+    assert ed["b_eps"] <= eps_cap and ed["A_eps"] <= eps_cap, ed
+    # dense A0 = structural A_0 scattered
+    rp, ci = g["pattern"]
+    A0 = np.zeros_like(g["A0"])
+    for i in range(n):
+        for e in range(rp[i], rp[i + 1]):
+            A0[:, i, ci[e]] = g["A"][:, 0, e]
+    assert np.array_equal(A0, g["A0"])
+    sv = H.solve_errors(sys_, x_np, out, g["dx"], F)
+    assert sv["dx"] <= 1, sv["dx"]
+    assert sv["dx_eps"] <= eps_cap * n, sv["dx_eps"]
+    xe = H.xnew_errors(sys_, x_np, out, g["x_new"], F, sv["s"])
+    assert xe <= 1, xe
+    # norms: ||b|| and ||dx|| against the oracle's, the residual is at rounding level
+    tol = synth.TOL_P[K]
+    nb = H.limbs_to_fraction(g["res"][:, 0])
+    assert abs(nb - H.to_frac(F, out["norm_b"])) <= Fraction(tol) * (abs(H.to_frac(F, out["norm_b"])) + Fraction(1e-300))
+    ndx = H.limbs_to_fraction(g["res"][:, 2])
+    assert abs(ndx - H.to_frac(F, out["norm_dx"])) <= Fraction(tol) * max(Fraction(float(max(sv["s"]))), abs(ndx))
+    nr = float(H.limbs_to_fraction(g["res"][:, 1]))
+    assert nr <= tol * float(max(sv["s"])) * n
+    assert g["status"] == 0
+    return g, out, ed, sv
+
+
+# ------------------------------------------------------------------ small / medium, all precisions
+def test_C1_exact_tier():
+    sys_ = synth.build_config("C1")
+    for kind in ("near", "start"):
+        x = synth.make_x(sys_, kind, seed=3)
+        _full_parity(sys_, x, O.ExactField())
+
+
+@pytest.mark.parametrize("K,n,D,seed", [(2, 40, 15, 1), (4, 36, 20, 2), (8, 34, 24, 3)])
+def test_medium_triangular(K, n, D, seed):
+    """spans two BS tiles (32 + ragged tail) and long monomials."""
+    sys_ = synth.triangular_system(n, D, K, seed=seed)
+    x = synth.make_x(sys_, "near", seed=seed + 10)
+    _full_parity(sys_, x, O.field_for(K))
+
+
+def test_two_column_banded():
+    sys_ = synth.banded_two_column_system(40, 8, 10, 4, seed=5)
+    x = synth.make_x(sys_, "near", seed=6)
+    _full_parity(sys_, x, O.field_for(4))
+
+
+@pytest.mark.parametrize("K", [2, 4, 8])
+def test_degenerate_shapes(K):
+    """n = 1 (m = 1 monomials only), D = 0 (one coefficient), a 2-variable system."""
+    for sys_ in (synth.triangular_system(1, 5, K, seed=1),
+                 synth.triangular_system(5, 0, K, seed=2),
+                 synth.custom_system([[[0, 1]], [[1]]], [1.0, 1.0], 4, K, [0.9, -0.95])):
+        x = synth.make_x(sys_, "near", seed=4)
+        _full_parity(sys_, x, O.field_for(K))
+
+
+# ------------------------------------------------------------------ bit-exact pins
+@pytest.mark.parametrize("K", [2, 4, 8])
+def test_integer_system_bit_exact(K):
+    """x_j = 1/(1-t) + integer perturbation: every b and A coefficient is an
+    integer < 2^53, so the GPU must reproduce the exact values bit for bit."""
+    sys_ = synth.inv1mt_system(8, 8, K, two_column=True)
+    x = synth.make_x(sys_, "int", seed=7)
+    g = _run_all(sys_, x)
+    F = O.ExactField()
+    b, A = O.evaluate(sys_, O.read_x(x, F), F)
+    rp, ci = g["pattern"]
+    for i in range(sys_.n):
+        for k in range(sys_.d):
+            assert b[i][k].denominator == 1 and abs(b[i][k]) < 2 ** 53
+            assert g["b"][0, k, i] == float(b[i][k]) and not g["b"][1:, k, i].any()
+            for e in range(rp[i], rp[i + 1]):
+                v = A[i][int(ci[e])][k]
+                assert g["A"][0, k, e] == float(v) and not g["A"][1:, k, e].any()
+
+
+@pytest.mark.parametrize("K", [2, 4, 8])
+def test_zero_rhs_gives_zero_update_bitwise(K):
+    """Eq.(11): at the exact 1/(1-t) solution b = 0 exactly, so
+    QR dx_k = 0 => dx = 0 bit for bit and x is unchanged."""
+    sys_ = synth.inv1mt_system(6, 7, K)
+    x = synth.make_x(sys_, "exact")
+    g = _run_all(sys_, x)
+    assert not g["b"].any()
+    assert not g["dx"].any()
+    assert np.array_equal(g["x_new"], x)
+
+
+# ------------------------------------------------------------------ Newton behaviour
+@pytest.mark.parametrize("K,n,D", [(2, 8, 8), (4, 8, 15), (8, 6, 31)])
+def test_quadratic_convergence_to_closed_form(K, n, D):
+    """Iterated GPU steps from 'start' (x_0 correct to half precision):
+    after i steps coefficients k <= 2^i - 2 match exp(alpha t) (SURVEY c.3), and
+    at the end every coefficient does, within tol_p of the coefficient scale."""
+    torch = _torch()
+    sys_ = synth.triangular_system(n, D, K, seed=11)
+    exact = synth.make_x(sys_, "exact")
+    x = torch.tensor(synth.make_x(sys_, "start", seed=12), device="cuda:0")
+    h = _handle(sys_)
+    tol = synth.TOL_P[K]
+    for it in range(1, 9):
+        h.step(x)
+        xn = _np(x)
+        good = min(2 ** it - 2, D)
+        for k in range(good + 1):
+            for j in range(n):
+                e = abs(H.limbs_to_fraction(xn[:, j, k]) - H.limbs_to_fraction(exact[:, j, k]))
+                scale = Fraction(max(abs(float(exact[0, j, k])), 1e-300))
+                # the rhs is rounded to md, so the attainable accuracy is ~n eps relative
+                assert e <= Fraction(tol) * scale * 64, (it, k, j, float(e / scale))
+        if good >= D:
+            break
+
+
+def test_fixed_point():
+    """From the rounded exact solution the update is at rounding level: ||dx|| <= tol."""
+    torch = _torch()
+    for K, n, D in ((2, 8, 8), (4, 16, 15), (8, 8, 31)):
+        sys_ = synth.triangular_system(n, D, K, seed=21)
+        x = torch.tensor(synth.make_x(sys_, "exact"), device="cuda:0")
+        res = torch.zeros((K, 3), dtype=torch.float64, device="cuda:0")
+        _handle(sys_).step(x, res)
+        r = _np(res)
+        assert abs(r[0, 2]) <= synth.TOL_P[K] * n   # ||dx||, coefficients are O(1)
+
+
+# ------------------------------------------------------------------ API semantics
+def test_reuse_qr_and_ledger():
+    import paper_2301_12659_b200 as P
+    torch = _torch()
+    sys_ = synth.triangular_system(16, 7, 4, seed=3)
+    h = _handle(sys_)
+    x = torch.tensor(synth.make_x(sys_, "start", seed=1), device="cuda:0")
+    with pytest.raises(P.NSError) as ei:
+        h.step(x, flags=P.NS_REUSE_QR)
+    assert ei.value.code == 10                              # NS_ESTATE
+    h.step(x, flags=P.NS_LEDGER)
+    h.step(x, flags=P.NS_LEDGER | P.NS_REUSE_QR)
+    led = h.ledger()
+    assert led["steps"] == 2 and led["qr_count"] == 1      # "QR once"
+    assert led["ms_convolution"] > 0 and led["ms_stage"] > 0
+    assert P.lib().ns_newton_series_step(h._h, 8, 16, 7, x.data_ptr(), None, 0, None) == 2   # NS_EPREC
+    assert P.lib().ns_newton_series_step(h._h, 4, 15, 7, x.data_ptr(), None, 0, None) == 3   # NS_EDIM
+
+
+def test_deterministic_step():
+    torch = _torch()
+    sys_ = synth.triangular_system(40, 15, 4, seed=9)
+    x0 = synth.make_x(sys_, "near", seed=2)
+    outs = []
+    for _ in range(2):
+        h = _handle(sys_)
+        x = torch.tensor(x0, device="cuda:0")
+        h.step(x)
+        outs.append(_np(x))
+    assert np.array_equal(outs[0], outs[1])
+
+
+# ------------------------------------------------------------------ batched (C5 shape)
+def test_batched_matches_oracle_and_is_batch_invariant():
+    torch = _torch()
+    K, n, D = 2, 32, 15
+    base = synth.build_config("C5")
+    B = 24
+    paths = [synth.triangular_system(n, D, K, seed=12665 + p) for p in range(B)]
+    xs = np.stack([synth.make_x(s, "near", seed=100 + p) for p, s in enumerate(paths)])
+    rhs = np.stack([s.rhs for s in paths])
+    h = _handle(base, max_batch=B)
+    X = torch.tensor(xs, device="cuda:0")
+    R = torch.tensor(rhs, device="cuda:0")
+    res = torch.zeros((B, K, 3), dtype=torch.float64, device="cuda:0")
+    h.step_batched(X, R, res)
+    Xn = _np(X)
+    # batch invariance: path 5 alone gives the same bits
+    X1 = torch.tensor(xs[5:6], device="cuda:0")
+    h.step_batched(X1, torch.tensor(rhs[5:6], device="cuda:0"))
+    assert np.array_equal(_np(X1)[0], Xn[5])
+    # oracle parity on sampled paths
+    F = O.field_for(K)
+    for p in (0, 5, B - 1):
+        out = O.step(paths[p], xs[p], F, split=True)
+        sc = O.scales(paths[p], xs[p])
+        dxf = np.array([[float(out["dx"][k][i]) for i in range(n)] for k in range(D + 1)])
+        s_k, _ = O.stage_scales(paths[p], xs[p], H.dense_A0_float(out["A"], n), dxf, sc["s_b"], sc["s_A"])
+        assert H.xnew_errors(paths[p], xs[p], out, Xn[p], F, s_k) <= 1
+        nb = H.limbs_to_fraction(_np(res)[p, :, 0])
+        assert abs(nb - H.to_frac(F, out["norm_b"])) <= Fraction(synth.TOL_P[K]) * abs(H.to_frac(F, out["norm_b"]))
+
+
+# ------------------------------------------------------------------ full BASELINE sizes
+@pytest.mark.slow
+def test_C2_full_parity():
+    """configs[1]: dim=64, degree 31, quad double -- the whole step against the full oracle."""
+    sys_ = synth.build_config("C2")
+    x = synth.make_x(sys_, "near", seed=1)
+    _full_parity(sys_, x, O.field_for(4))
+
+
+@pytest.mark.slow
+def test_C3_sampled_parity():
+    """configs[2]: dim=128, degree 63, octo double.  Sampled rows of b and A
+    against the oracle; |R_jj| against the Cholesky factor of A0^T A0 (unique,
+    unlike Q and R); dx through the residual of the block system on sampled rows
+    with the GPU's verified A and b, evaluated exactly."""
+    sys_ = synth.build_config("C3")
+    x = synth.make_x(sys_, "near", seed=1)
+    g = _run_all(sys_, x)
+    F = O.field_for(8)
+    rows = [0, 1, 2, 63, 127]
+    ed = H.eval_diff_errors(sys_, x, g["b"], g["A"], rows, F, g["pattern"])
+    assert ed["b"] <= 1 and ed["A"] <= 1, ed
+    n, d, K = sys_.n, sys_.d, 8
+    # |R_jj| = diag of the Cholesky factor of A0^T A0
+    A0 = [[F.from_limbs(g["A0"][:, i, j]) for j in range(n)] for i in range(n)]
+    G = [[sum((A0[r][i] * A0[r][j] for r in range(n)), F.zero) for j in range(n)] for i in range(n)]
+    L = F.ctx.cholesky(F.ctx.matrix(G))
+    for j in range(n):
+        rj = abs(H.limbs_to_fraction(g["rdiag"][:, j]))
+        lj = H.to_frac(F, L[j, j])
+        assert abs(rj - lj) <= Fraction(synth.TOL_P[K]) * lj * n
+    # block-system residual of the GPU dx on sampled rows, exact arithmetic on GPU A, b
+    rp, ci = g["pattern"]
+    tol = synth.TOL_P[K]
+    for i in (0, 64, 127):
+        for k in range(0, d, 7):
+            r = H.limbs_to_fraction(g["b"][:, k, i])
+            scale = abs(r)
+            for j in range(k + 1):
+                for e in range(rp[i], rp[i + 1]):
+                    t = H.limbs_to_fraction(g["A"][:, j, e]) * H.limbs_to_fraction(g["dx"][:, k - j, ci[e]])
+                    r -= t
+                    scale += abs(t)
+            assert abs(r) <= Fraction(tol) * scale, (i, k, float(abs(r) / scale))
