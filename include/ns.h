@@ -129,6 +129,11 @@ ns_status ns_get_r_diag(ns_system* sys, double* rdiag, void* stream);
 ns_status ns_md_op(int precision, int op, int n, const double* a, const double* b, double* c,
                    void* stream);
 
+/* FP64 pipe microbenchmark: op 0 = DFMA chains, 1 = DADD chains on
+ * every SM; writes the achieved rate in G instructions/s and the kernel time.
+ * Synchronises the device (measurement entry, not part of the step). */
+ns_status ns_fp64_peak_probe(int device, int op, double* ginstr_per_s, double* ms);
+
 /* Synchronises the handle's last stream and returns the device status word. */
 ns_status ns_get_status(ns_system* sys, ns_step_info* host_out);
 /* Synchronises; per-class milliseconds accumulated over steps run with NS_LEDGER. */

@@ -30,7 +30,8 @@ STATUS = {0: "NS_OK", 1: "NS_EINVAL", 2: "NS_EPREC", 3: "NS_EDIM", 4: "NS_EMONO"
 EXPORTS = ["ns_system_create", "ns_system_destroy", "ns_newton_series_step",
            "ns_newton_series_step_batched", "ns_eval_diff", "ns_nnz", "ns_jacobian_pattern",
            "ns_toeplitz_solve", "ns_get_r_diag", "ns_md_op", "ns_get_status", "ns_get_ledger",
-           "ns_reset_ledger", "ns_last_launch_count", "ns_strerror", "ns_build_info"]
+           "ns_reset_ledger", "ns_last_launch_count", "ns_strerror", "ns_build_info",
+           "ns_fp64_peak_probe"]
 
 
 class NSError(RuntimeError):
@@ -90,6 +91,8 @@ def lib() -> ctypes.CDLL:
         "ns_last_launch_count": ([vp], i32),
         "ns_strerror": ([ctypes.c_int], ctypes.c_char_p),
         "ns_build_info": ([], ctypes.c_char_p),
+        "ns_fp64_peak_probe": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -254,3 +257,11 @@ def md_op(precision: int, op: str, a, b=None, c=None, stream=None):
 
 def build_info() -> str:
     return lib().ns_build_info().decode()
+
+
+def fp64_peak_probe(device: int = 0, op: str = "dfma") -> dict:
+    """Measured FP64 pipe rate (G instructions/s) of DFMA or DADD chains on all SMs."""
+    g, ms = ctypes.c_double(), ctypes.c_double()
+    _check(lib().ns_fp64_peak_probe(device, 0 if op == "dfma" else 1, ctypes.byref(g), ctypes.byref(ms)),
+           "ns_fp64_peak_probe")
+    return {"ginstr_per_s": g.value, "ms": ms.value}

@@ -32,43 +32,59 @@ template <int K>
 ns_status step_impl(ns_system* s, double* x, double* res_out, uint32_t flags, cudaStream_t st) {
   const bool ledger = (flags & NS_LEDGER) != 0;
   s->last_launches = 0;
-  if (ledger) CK(cudaEventRecord(s->ev[0], st));
+  cudaEvent_t* ev = nullptr;
+  if (ledger) {
+    if (s->ledger_count == ns_system::LRING) {  // ring full: read the oldest record (rare)
+      ns_status r0 = collect_one(s);
+      if (r0) return r0;
+    }
+    ev = s->ev[(s->ledger_head + s->ledger_count) % ns_system::LRING];
+    CK(cudaEventRecord(ev[0], st));
+  }
   ns_status r = Impl<K>::evaldiff(s, x, st);
   if (r) return r;
-  if (ledger) CK(cudaEventRecord(s->ev[1], st));
+  if (ledger) CK(cudaEventRecord(ev[1], st));
   if (!(flags & NS_REUSE_QR)) {
     r = Impl<K>::qr(s, st);
     if (r) return r;
   }
-  if (ledger) CK(cudaEventRecord(s->ev[2], st));
+  if (ledger) CK(cudaEventRecord(ev[2], st));
   r = Impl<K>::stage(s, 0, st);
   if (r) return r;
-  if (ledger) CK(cudaEventRecord(s->ev[3], st));
+  if (ledger) CK(cudaEventRecord(ev[3], st));
   r = Impl<K>::residual(s, x, res_out, st);
   if (r) return r;
   if (ledger) {
-    CK(cudaEventRecord(s->ev[4], st));
-    s->ledger_pending = true;
+    CK(cudaEventRecord(ev[4], st));
+    s->ledger_count += 1;
     if (!(flags & NS_REUSE_QR)) s->ledger.qr_count += 1;
   }
   s->last_stream = st;
   return NS_OK;
 }
 
-ns_status collect_ledger(ns_system* s) {
-  if (!s->ledger_pending) return NS_OK;
-  CK(cudaEventSynchronize(s->ev[4]));
+ns_status collect_one(ns_system* s) {
+  cudaEvent_t* ev = s->ev[s->ledger_head];
+  CK(cudaEventSynchronize(ev[4]));
   float ms[4];
-  for (int i = 0; i < 4; ++i) CK(cudaEventElapsedTime(&ms[i], s->ev[i], s->ev[i + 1]));
+  for (int i = 0; i < 4; ++i) CK(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
   s->ledger.ms_convolution += ms[0];
   s->ledger.ms_qr += ms[1];
   s->ledger.ms_stage += ms[2];
   s->ledger.ms_residual += ms[3];
   s->ledger.steps += 1;
-  s->ledger_pending = false;
+  s->ledger_head = (s->ledger_head + 1) % ns_system::LRING;
+  s->ledger_count -= 1;
   return NS_OK;
 }
 
+ns_status collect_ledger(ns_system* s) {
+  while (s->ledger_count > 0) {
+    ns_status r = collect_one(s);
+    if (r) return r;
+  }
+  return NS_OK;
+}
 
 void free_all(ns_system* s) {
   void* ptrs[] = {s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst, s->row_ptr, s->col_idx, s->job_order,
@@ -77,8 +93,9 @@ void free_all(ns_system* s) {
                   s->bar, s->status, s->bws};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  for (auto& e : s->ev)
-    if (e) cudaEventDestroy(e);
+  for (auto& row : s->ev)
+    for (auto& e : row)
+      if (e) cudaEventDestroy(e);
 }
 
 }  // namespace
@@ -235,7 +252,8 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= cudaMemcpy(s->rhs, desc->rhs, sizeof(double) * K * n * d, cudaMemcpyHostToDevice) == cudaSuccess;
   ok &= cudaMemset(s->status, 0, sizeof(unsigned)) == cudaSuccess;
   ok &= cudaMemset(s->bar, 0, 4 * sizeof(unsigned)) == cudaSuccess;
-  for (auto& e : s->ev) ok &= cudaEventCreate(&e) == cudaSuccess;
+  for (auto& row : s->ev)
+    for (auto& e : row) ok &= cudaEventCreate(&e) == cudaSuccess;
   if (!ok) return fail(NS_ECUDA);
   *out = s;
   return NS_OK;
@@ -257,10 +275,6 @@ ns_status ns_newton_series_step(ns_system* s, int precision, int dim, int degree
   if (flags & ~(NS_REUSE_QR | NS_NO_RESIDUAL | NS_LEDGER)) return NS_EINVAL;
   if ((flags & NS_REUSE_QR) && !s->qr_cached) return NS_ESTATE;
   cudaStream_t st = (cudaStream_t)stream;
-  if (flags & NS_LEDGER) {
-    ns_status r = collect_ledger(s);
-    if (r) return r;
-  }
   switch (s->K) {
     case 2: return step_impl<2>(s, x, res_out, flags, st);
     case 4: return step_impl<4>(s, x, res_out, flags, st);
@@ -383,4 +397,56 @@ extern "C" ns_status ns_md_op(int precision, int op, int n, const double* a, con
     case 8: return Impl<8>::md_op(op, n, a, b, c, st);
     default: return NS_EPREC;
   }
+}
+
+// ------------------------------------------------------------------ FP64 peak probe
+namespace {
+__global__ void __launch_bounds__(256) fp64_probe_kernel(int op, int iters, double seed, double* sink) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = seed + threadIdx.x * 1e-9 + i * 1e-12;
+  const double m = 0.999999999, c = 1e-300;
+  if (op == 0) {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = __fma_rn(a[i], m, c);
+    }
+  } else {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = __dadd_rn(a[i], c);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 12345.678) sink[0] = s;  // keep the chains alive
+}
+}  // namespace
+
+extern "C" ns_status ns_fp64_peak_probe(int device, int op, double* ginstr, double* ms_out) {
+  if (!ginstr || (op != 0 && op != 1)) return NS_EINVAL;
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  double* sink = nullptr;
+  CK(cudaMalloc(&sink, sizeof(double)));
+  const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 4096;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  fp64_probe_kernel<<<blocks, threads>>>(op, iters, 1.0, sink);  // warm-up
+  CK(cudaEventRecord(e0));
+  for (int r = 0; r < 5; ++r) fp64_probe_kernel<<<blocks, threads>>>(op, iters, 1.0, sink);
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  const double instr = 5.0 * blocks * threads * (double)iters * 8.0;
+  *ginstr = instr / (ms * 1e-3) * 1e-9;
+  if (ms_out) *ms_out = ms / 5.0;
+  return NS_OK;
 }

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(128) householder_qr_kernel(int n, const double
       make_reflector<K>(n, look, W, vhead, beta, rdiag, status);
     }
     for (int c = gw; c < ncol; c += nw) {
-      if (c > j && c != look) apply_reflector<K>(n, j, c, W, vhead, beta);
+      if (c > j && (c != look || look >= n)) apply_reflector<K>(n, j, c, W, vhead, beta);
     }
     grid_sync(bar);
   }

@@ -29,8 +29,9 @@ struct ns_system {
   bool qr_cached = false;
   cudaStream_t last_stream = nullptr;
   // ledger
-  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-  bool ledger_pending = false;
+  static constexpr int LRING = 64;           // pending ledger records (5 events each)
+  cudaEvent_t ev[LRING][5] = {};
+  int ledger_head = 0, ledger_count = 0;     // ring of steps whose events are not yet read
   ns_ledger ledger{};
   int last_launches = 0;
   // batched

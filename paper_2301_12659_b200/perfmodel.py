@@ -1,0 +1,74 @@
+"""Work accounting for one Newton step: exact md-operation
+counts per kernel class from the system structure, and the static FP64
+instruction mix of this library's md routines (counted from csrc/md.cuh; the
+ncu cross-check is in profiles/).  Host-side bookkeeping only.
+
+Numerators (always labelled):
+  md_fma      algorithmic md multiply-adds (triangular convolutions, no padding)
+  fp64_flops  md_fma x (DADD + DMUL + 2 DFMA) of our md_fma   -> "FP64 GFLOPS"
+  fp64_instr  md_fma x (DADD + DMUL + DFMA) instructions      -> FP64-pipe fraction
+  paper_flops md_mul x T2 cost (23/336/1742), context only (non-FMA counts)
+"""
+from __future__ import annotations
+
+# FP64 instructions of one md fused accumulate r = acc + a*b (csrc/md.cuh fma_acc)
+#   K=2: two_prod (DMUL+DFMA) + 2 DFMA + two_sum (6) + 2 DADD + fast_two_sum (3)
+#   K=4: 20 two_sum + 12 DADD + 6 two_prod + 4 DFMA       (cascade 14 + renorm 6)
+#   K=8: 154 two_sum + 56 DADD + 28 two_prod + 8 DFMA     (cascade 140 + renorm 14)
+MD_FMA_MIX = {
+    2: dict(dadd=11, dmul=1, dfma=3),
+    4: dict(dadd=20 * 6 + 12, dmul=6, dfma=6 + 4),
+    8: dict(dadd=154 * 6 + 56, dmul=28, dfma=28 + 8),
+}
+# md add: K(K-1)/2 cascade two_sum + K DADD + renorm 2(K-1) two_sum (K=2 specialised: 11)
+MD_ADD_MIX = {2: dict(dadd=11, dmul=0, dfma=0),
+              4: dict(dadd=12 * 6 + 4, dmul=0, dfma=0),
+              8: dict(dadd=42 * 6 + 8, dmul=0, dfma=0)}
+T2_MUL = {2: 23, 4: 336, 8: 1742}
+
+
+def mix_flops(m):
+    return m["dadd"] + m["dmul"] + 2 * m["dfma"]
+
+
+def mix_instr(m):
+    return m["dadd"] + m["dmul"] + m["dfma"]
+
+
+def products(m: int) -> int:
+    return 0 if m <= 1 else (1 if m == 2 else 3 * m - 5)
+
+
+def step_counts(eq_ptr, mono_ptr, nnz: int, n: int, d: int, TB: int = 32) -> dict:
+    """md multiply-adds per kernel class of one step (all orders 0..D)."""
+    M = len(mono_ptr) - 1
+    S = sum(products(int(mono_ptr[t + 1] - mono_ptr[t])) for t in range(M))
+    conv = S * d * (d + 1) // 2                        # a2-a4: triangular convolutions
+    scale = (M + sum(int(mono_ptr[t + 1] - mono_ptr[t]) for t in range(M))) * d   # a5
+    qr = sum((n - j) + 2 * (2 * n - j - 1) * (n - j) for j in range(n))           # a6 on [A0 | I]
+    updates = nnz * d * (d - 1) // 2                     # a7
+    qhb = n * n * d                                      # a8 (explicit Q^T)
+    T = (n + TB - 1) // TB
+    bs = 0
+    for t in range(T):                                   # a9 per stage
+        t0, t1 = t * TB, min(n, (t + 1) * TB)
+        bs += (t1 - t0) * (n - t1) + (t1 - t0) * (t1 - t0)
+    bs *= d
+    resid = n * n * d                                    # a10 dense A0 dx_k
+    return dict(convolution=conv + scale, conv_products=conv, qr=qr, updates=updates, qhb=qhb, bs=bs,
+                stage=updates + qhb + bs, residual=resid, series_products=S)
+
+
+def flops(md_fma: int, K: int) -> int:
+    return md_fma * mix_flops(MD_FMA_MIX[K])
+
+
+def instr(md_fma: int, K: int) -> int:
+    return md_fma * mix_instr(MD_FMA_MIX[K])
+
+
+def fp64_peak_gflops(sm_count: int = 148, mhz: float = 1965.0) -> dict:
+    """Derived FP64 peak (B200_PROFILING.md: 148 SMs; 64 FP64 lanes/SM/clk;
+    sm_max_mhz from MEASURED_PEAKS.json): FMA-counted flops and pipe instructions."""
+    lanes = sm_count * 64
+    return dict(gflops=lanes * 2 * mhz * 1e-3, ginstr=lanes * mhz * 1e-3)
