@@ -28,6 +28,8 @@ int cost_of_eq(const ns_system* s, int i) {
   return (int)std::min<long long>(c, 1 << 30);
 }
 
+ns_status collect_one(ns_system* s);
+
 template <int K>
 ns_status step_impl(ns_system* s, double* x, double* res_out, uint32_t flags, cudaStream_t st) {
   const bool ledger = (flags & NS_LEDGER) != 0;
