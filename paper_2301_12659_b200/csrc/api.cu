@@ -91,7 +91,7 @@ ns_status collect_ledger(ns_system* s) {
 void free_all(ns_system* s) {
   void* ptrs[] = {s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst, s->row_ptr, s->col_idx, s->job_order,
                   s->coeff, s->rhs, s->b, s->A, s->A0, s->W, s->vhead, s->beta, s->rdiag, s->R, s->Qt,
-                  s->invR, s->bp, s->dx, s->y, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
+                  s->invR, s->bp, s->dx, s->y, s->part, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
                   s->bar, s->status, s->bws};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -223,6 +223,12 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->bp, (size_t)K * d * n) == cudaSuccess;
   ok &= dalloc(&s->dx, (size_t)K * d * n) == cudaSuccess;
   ok &= dalloc(&s->y, (size_t)K * n) == cudaSuccess;
+  {
+    int maxlen = 1;
+    for (int i = 0; i < n; ++i) maxlen = std::max(maxlen, s->h_row_ptr[i + 1] - s->h_row_ptr[i]);
+    s->cmax = std::max(1, (std::max(1, (int)d - 1) * maxlen + 63) / 64);  // ns::UCH = 64
+    ok &= dalloc(&s->part, (size_t)K * n * s->cmax) == cudaSuccess;
+  }
   ok &= dalloc(&s->rbuf, (size_t)K * d * n) == cudaSuccess;
   ok &= dalloc(&s->knorm, (size_t)3 * K * d) == cudaSuccess;
   ok &= dalloc(&s->res_tmp, (size_t)K * 3) == cudaSuccess;

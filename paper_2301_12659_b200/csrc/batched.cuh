@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, 
       md::mdv<K> inv_d = md::zero<K>();
       if (lane < nb) {
         md::mdv<K> rqq = md::load<K>(W, lsW, (long long)(t0 + lane) * n + t0 + lane);
-        inv_d = md::div<K>(md::from_double<K>(1.0), rqq);
+        inv_d = md::recip<K>(rqq);
       }
       md::mdv<K> Xc = md::zero<K>();
       if (cl < nb) {

@@ -1,6 +1,7 @@
 // impl.cuh -- per-precision launchers (instantiated once per K in kernels_k{2,4,8}.cu).
 #pragma once
 #include <algorithm>
+#include <cstdlib>
 
 #include "batched.cuh"
 #include "evaldiff.cuh"
@@ -51,7 +52,7 @@ ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
   CK(cudaMemsetAsync(s->dx, 0, sizeof(double) * (size_t)K * s->d * s->n, st));
   DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
             s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
-  ns::StageArgs a{s->b, s->A, s->Qt, s->R, s->invR, s->bp, s->dx, s->y, s->TB, k_lo};
+  ns::StageArgs a{s->b, s->A, s->Qt, s->R, s->invR, s->bp, s->dx, s->y, s->part, s->cmax, s->TB, k_lo};
   unsigned* bar = s->bar + 2;
   void* args[] = {&ds, &a, &bar};
   CK(cudaLaunchCooperativeKernel((const void*)ns::stage_kernel<K>, dim3(s->grid_st), dim3(128), args, 0, st));
@@ -76,10 +77,14 @@ ns_status setup_grids(ns_system* s) {
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::householder_qr_kernel<K>, 128, 0));
   if (occ < 1) return NS_ECUDA;
-  s->grid_qr = s->sms;  // one CTA per SM: a cheaper barrier than occ * sms
+  // cooperative grids: enough warps for the 2n columns of [A0 | I], never more
+  // CTAs than SMs (a grid barrier costs more with every CTA); env overrides for tuning
+  s->grid_qr = std::min(s->sms, std::max(1, (2 * s->n + 3) / 4));
+  if (const char* e = getenv("NS_QR_GRID")) s->grid_qr = std::max(1, std::min(s->sms * occ, atoi(e)));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::stage_kernel<K>, 128, 0));
   if (occ < 1) return NS_ECUDA;
   s->grid_st = s->sms;
+  if (const char* e = getenv("NS_STAGE_GRID")) s->grid_st = std::max(1, std::min(s->sms * occ, atoi(e)));
   s->ed_smem = sizeof(double) * (size_t)K * s->d;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::evaldiff_kernel<K>, 256, s->ed_smem));
   if (occ < 1) return NS_ECUDA;

@@ -215,37 +215,67 @@ MD_INL mdv<2> add<2>(const mdv<2>& a, const mdv<2>& b) {
 }
 
 // ---------------------------------------------------------------- division, sqrt
-// q = a / b by long division: q_i = r_0 / b_0, r -= q_i b, i = 0..K, then
-// renormalize the K+1 partial quotients (reading R23).
-template <int K>
-MD_INL mdv<K> div(const mdv<K>& a, const mdv<K>& b) {
-  double q[K + 1];
-  mdv<K> r = a;
-  const mdv<K> nb = neg<K>(b);
+// Newton iterations with precision doubling (reading R23): the K-limb result
+// refines the K/2-limb one, so the early iterations run in cheaper (shorter
+// latency) arithmetic; each iteration is two or three fused accumulates.
+template <int P, int K>
+MD_INL mdv<P> trunc(const mdv<K>& a) {
+  mdv<P> r;
 #pragma unroll
-  for (int i = 0; i <= K; ++i) {
-    q[i] = r.x[0] / b.x[0];
-    if (i < K) r = fma_acc<K>(r, from_double<K>(q[i]), nb);
-  }
-  return renorm<K, K + 1>(q);
+  for (int i = 0; i < P; ++i) r.x[i] = (i < K) ? a.x[i] : 0.0;
+  return r;
 }
 
-// sqrt(a), a >= 0: Newton y <- y + (a - y^2) / (2 y) from the hardware sqrt of
-// the leading limb; each step doubles the correct bits (reading R23).
+// 1/b: y <- y + y (1 - b y)
+template <int K>
+MD_INL mdv<K> recip(const mdv<K>& b) {
+  mdv<K> y;
+  if constexpr (K == 2) {
+    y = from_double<2>(1.0 / b.x[0]);
+  } else {
+    y = trunc<K, K / 2>(recip<K / 2>(trunc<K / 2, K>(b)));
+  }
+  mdv<K> e = fma_acc<K>(from_double<K>(1.0), neg<K>(b), y);  // 1 - b y
+  return fma_acc<K>(y, y, e);
+}
+
+// 1/sqrt(a), a > 0: y <- y + (y/2) (1 - a y^2)
+template <int K>
+MD_INL mdv<K> rsqrt(const mdv<K>& a) {
+  mdv<K> y;
+  if constexpr (K == 2) {
+    y = from_double<2>(1.0 / ::sqrt(a.x[0]));
+  } else {
+    y = trunc<K, K / 2>(rsqrt<K / 2>(trunc<K / 2, K>(a)));
+  }
+  mdv<K> t = mul<K>(y, y);
+  mdv<K> e = fma_acc<K>(from_double<K>(1.0), neg<K>(a), t);  // 1 - a y^2
+  mdv<K> h;
+#pragma unroll
+  for (int i = 0; i < K; ++i) h.x[i] = 0.5 * y.x[i];
+  return fma_acc<K>(y, h, e);
+}
+
+// a / b = q + y (a - q b), q = a y, y = 1/b (Markstein correction)
+template <int K>
+MD_INL mdv<K> div(const mdv<K>& a, const mdv<K>& b) {
+  const mdv<K> y = recip<K>(b);
+  const mdv<K> q = mul<K>(a, y);
+  const mdv<K> r = fma_acc<K>(a, neg<K>(q), b);
+  return fma_acc<K>(q, y, r);
+}
+
+// sqrt(a), a >= 0: s = a y, s + (y/2)(a - s^2), y = 1/sqrt(a) (Karp-Markstein)
 template <int K>
 MD_INL mdv<K> sqrt(const mdv<K>& a) {
   if (!(a.x[0] > 0.0)) return zero<K>();
-  mdv<K> y = from_double<K>(::sqrt(a.x[0]));
-  constexpr int IT = (K == 2) ? 1 : ((K == 4) ? 2 : 3);
+  const mdv<K> y = rsqrt<K>(a);
+  const mdv<K> s0 = mul<K>(a, y);
+  const mdv<K> r = fma_acc<K>(a, neg<K>(s0), s0);
+  mdv<K> h;
 #pragma unroll
-  for (int it = 0; it <= IT; ++it) {
-    mdv<K> res = fma_acc<K>(a, y, neg<K>(y));  // a - y^2
-    mdv<K> two_y = y;
-#pragma unroll
-    for (int i = 0; i < K; ++i) two_y.x[i] = 2.0 * y.x[i];
-    y = add<K>(y, div<K>(res, two_y));
-  }
-  return y;
+  for (int i = 0; i < K; ++i) h.x[i] = 0.5 * y.x[i];
+  return fma_acc<K>(s0, h, r);
 }
 
 // sign of an md value (leading nonzero limb decides; limbs are nonoverlapping)

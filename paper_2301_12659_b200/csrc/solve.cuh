@@ -53,7 +53,7 @@ __device__ void make_reflector(int n, int j, double* W, double* vhead, double* b
   md::mdv<K> bt = md::zero<K>();
   if (!md::is_zero<K>(sig)) {
     // v^T v = -2 alpha v0, beta = 2 / v^T v = -1 / (alpha v0)
-    bt = md::neg<K>(md::div<K>(md::from_double<K>(1.0), md::mul<K>(alpha, v0)));
+    bt = md::neg<K>(md::recip<K>(md::mul<K>(alpha, v0)));
   } else if (lane == 0 && status) {
     atomicOr(status, ST_SINGULAR);
   }
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256) invert_tiles_kernel(int n, int TB, const 
   md::mdv<K> inv_d = md::zero<K>();
   if (lane < nb) {
     md::mdv<K> rqq = md::load<K>(R, lsR, (long long)(t0 + lane) * n + t0 + lane);
-    inv_d = md::div<K>(md::from_double<K>(1.0), rqq);
+    inv_d = md::recip<K>(rqq);
   }
   for (int c = threadIdx.x >> 5; c < TB; c += blockDim.x >> 5) {  // column of the inverse
     md::mdv<K> X = md::zero<K>();  // lane q holds X[q][c]
@@ -198,9 +198,13 @@ struct StageArgs {
   double* bp;          // [K][d][n]  b'_k
   double* dx;          // [K][d][n]
   double* y;           // [K][n]
+  double* part;        // [K][n][cmax] partial sums of the update chunks
+  int cmax;            // max chunks per row = ceil((d-1) * maxlen / UCH)
   int TB;
   int k_lo;
 };
+
+constexpr int UCH = 64;  // update terms per chunk (32 lanes x 2)
 
 template <int K>
 __global__ void __launch_bounds__(128) stage_kernel(DevSys s, StageArgs a, unsigned* bar) {
@@ -213,23 +217,50 @@ __global__ void __launch_bounds__(128) stage_kernel(DevSys s, StageArgs a, unsig
   const int T = (n + TB - 1) / TB;
   const long long lsI = (long long)T * TB * TB;
   for (int k = a.k_lo; k < d; ++k) {
-    // ---- updates: b'_k = b_k - sum_{j=1}^{k} A_j dx_{k-j}
-    for (int i = gw; i < n; i += nw) {
-      const int r0 = s.row_ptr[i], len = s.row_ptr[i + 1] - r0;
-      md::mdv<K> acc = md::zero<K>();
-      const int tot = (k - a.k_lo) * len;  // stages below k_lo are inactive (dx = 0)
-      for (int t = lane; t < tot; t += 32) {
-        const int j = 1 + t / len;
-        const int e = r0 + t % len;
-        md::mdv<K> aij = md::load<K>(a.A + (long long)j * nnz, lsA, e);
-        md::mdv<K> xv = md::load_cg<K>(a.dx + (long long)(k - j) * n, lsV, s.col_idx[e]);
-        acc = md::fma_acc<K>(acc, aij, xv);
+    // ---- updates: b'_k = b_k - sum_{j=1}^{k} A_j dx_{k-j}.  The k*len_i terms
+    // of row i are cut into chunks of UCH; (row, chunk) slots are dealt to all
+    // warps, each chunk is summed by one warp (fixed lane order + butterfly),
+    // then the chunks of a row are summed in chunk order: deterministic and
+    // balanced whatever the row lengths.
+    const int kk = k - a.k_lo;  // stages below k_lo are inactive (dx = 0)
+    if (kk > 0) {
+      int maxlen = 0;
+      for (int i = lane; i < n; i += 32) maxlen = max(maxlen, s.row_ptr[i + 1] - s.row_ptr[i]);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
+      const int cpr = (kk * maxlen + UCH - 1) / UCH;  // chunk slots per row
+      const long long lsP = (long long)n * a.cmax;
+      for (long long slot = gw; slot < (long long)n * cpr; slot += nw) {
+        const int i = (int)(slot / cpr), c = (int)(slot % cpr);
+        const int r0 = s.row_ptr[i], len = s.row_ptr[i + 1] - r0;
+        const int tot = kk * len;
+        if (c * UCH >= tot) continue;  // empty slot (short row), warp-uniform
+        md::mdv<K> acc = md::zero<K>();
+        for (int t = c * UCH + lane; t < min(tot, (c + 1) * UCH); t += 32) {
+          const int j = 1 + t / len;
+          const int e = r0 + t % len;
+          md::mdv<K> aij = md::load<K>(a.A + (long long)j * nnz, lsA, e);
+          md::mdv<K> xv = md::load_cg<K>(a.dx + (long long)(k - j) * n, lsV, s.col_idx[e]);
+          acc = md::fma_acc<K>(acc, aij, xv);
+        }
+        acc = md::group_sum<K>(acc, 32);
+        if (lane == 0) md::store_cg<K>(a.part, lsP, (long long)i * a.cmax + c, acc);
       }
-      acc = md::group_sum<K>(acc, 32);
-      if (lane == 0) {
-        md::mdv<K> bk = md::load<K>(a.b + (long long)k * n, lsV, i);
-        md::store_cg<K>(a.bp + (long long)k * n, lsV, i, md::sub<K>(bk, acc));
+      grid_sync(bar);
+      for (int i = gw; i < n; i += nw) {
+        const int len = s.row_ptr[i + 1] - s.row_ptr[i];
+        const int nc = (kk * len + UCH - 1) / UCH;
+        md::mdv<K> acc = md::zero<K>();
+        for (int c = lane; c < nc; c += 32) acc = md::add<K>(acc, md::load_cg<K>(a.part, lsP, (long long)i * a.cmax + c));
+        acc = md::group_sum<K>(acc, 32);
+        if (lane == 0) {
+          md::mdv<K> bk = md::load<K>(a.b + (long long)k * n, lsV, i);
+          md::store_cg<K>(a.bp + (long long)k * n, lsV, i, md::sub<K>(bk, acc));
+        }
       }
+    } else {
+      for (int i = gw; i < n; i += nw)
+        if (lane == 0) md::store_cg<K>(a.bp + (long long)k * n, lsV, i, md::load<K>(a.b + (long long)k * n, lsV, i));
     }
     grid_sync(bar);
     // ---- qhb: y = Q^T b'_k

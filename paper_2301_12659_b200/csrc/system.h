@@ -20,6 +20,8 @@ struct ns_system {
   // workspace
   double *b = nullptr, *A = nullptr, *A0 = nullptr, *W = nullptr, *vhead = nullptr, *beta = nullptr;
   double *rdiag = nullptr, *R = nullptr, *Qt = nullptr, *invR = nullptr, *bp = nullptr, *dx = nullptr;
+  double *part = nullptr;
+  int cmax = 1;
   double *y = nullptr, *rbuf = nullptr, *knorm = nullptr, *res_tmp = nullptr, *ws = nullptr;
   int* job_counter = nullptr;
   unsigned* bar = nullptr;     // [4]: qr barrier, stage barrier
