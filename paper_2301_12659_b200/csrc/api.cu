@@ -92,7 +92,8 @@ void free_all(ns_system* s) {
   void* ptrs[] = {s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst, s->row_ptr, s->col_idx, s->job_order,
                   s->coeff, s->rhs, s->b, s->A, s->A0, s->W, s->vhead, s->beta, s->rdiag, s->R, s->Qt,
                   s->invR, s->bp, s->dx, s->y, s->part, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
-                  s->bar, s->status, s->bws};
+                  s->bar, s->status, s->bws, s->jobs, s->ser_off, s->pool, s->prog, s->left,
+                  s->left_init};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& row : s->ev)
@@ -189,6 +190,35 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   std::stable_sort(s->h_job_order.begin(), s->h_job_order.end(),
                    [&](int a, int b) { return cost[a] > cost[b]; });
 
+  // eval/diff job queue (see evaldiff.cuh): chains longest first, cross products by
+  // the layer their inputs appear at, equations by their longest monomial
+  std::vector<int4> chains, cross, eqs;
+  std::vector<long long> ser_off(M, 0);
+  std::vector<int> left(M, 0);
+  long long pool_series = 0;
+  auto prod = [](int m) { return m <= 1 ? 0 : (m == 2 ? 1 : 3 * m - 5); };
+  for (int t = 0; t < M; ++t) {
+    const int m = s->h_mono_ptr[t + 1] - s->h_mono_ptr[t];
+    ser_off[t] = pool_series;
+    pool_series += prod(m);
+    if (m >= 2) chains.push_back(make_int4(0, t, m - 1, 0));
+    if (m >= 3) chains.push_back(make_int4(1, t, m - 2, 0));
+    for (int j = 2; j <= m - 1; ++j) cross.push_back(make_int4(2, t, j, std::max(j - 2, m - j - 1)));
+    left[t] = (m <= 1) ? 0 : (m == 2 ? 1 : m);
+  }
+  for (int i = 0; i < n; ++i) {
+    int mm = 0;
+    for (int t = s->h_eq_ptr[i]; t < s->h_eq_ptr[i + 1]; ++t) mm = std::max(mm, s->h_mono_ptr[t + 1] - s->h_mono_ptr[t]);
+    eqs.push_back(make_int4(3, i, 0, mm));
+  }
+  std::stable_sort(chains.begin(), chains.end(), [](int4 a, int4 b) { return a.z > b.z; });
+  std::stable_sort(cross.begin(), cross.end(), [](int4 a, int4 b) { return a.w < b.w; });
+  std::stable_sort(eqs.begin(), eqs.end(), [](int4 a, int4 b) { return a.w < b.w; });
+  std::vector<int4> jobs(chains);
+  jobs.insert(jobs.end(), cross.begin(), cross.end());
+  jobs.insert(jobs.end(), eqs.begin(), eqs.end());
+  s->njobs = (int)jobs.size();
+
   ns_status st = NS_OK;
   auto fail = [&](ns_status e) {
     free_all(s);
@@ -242,7 +272,18 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
     default: st = Impl<8>::setup(s); break;
   }
   if (st) return fail(st);
-  if (dalloc(&s->ws, (size_t)s->grid_ed * 3 * s->m_max * K * d) != cudaSuccess) return fail(NS_ENOMEM);
+  ok = true;
+  ok &= dalloc(&s->jobs, jobs.size()) == cudaSuccess;
+  ok &= dalloc(&s->ser_off, M) == cudaSuccess;
+  ok &= dalloc(&s->pool, (size_t)std::max<long long>(1, pool_series) * K * d) == cudaSuccess;
+  ok &= dalloc(&s->prog, 2 * (size_t)M) == cudaSuccess;
+  ok &= dalloc(&s->left, M) == cudaSuccess;
+  ok &= dalloc(&s->left_init, M) == cudaSuccess;
+  if (!ok) return fail(NS_ENOMEM);
+  ok &= cudaMemcpy(s->jobs, jobs.data(), sizeof(int4) * jobs.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(s->ser_off, ser_off.data(), sizeof(long long) * M, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(s->left_init, left.data(), sizeof(int) * M, cudaMemcpyHostToDevice) == cudaSuccess;
+  if (!ok) return fail(NS_ECUDA);
   // upload
   std::vector<double> coeff((size_t)K * M, 0.0);
   if (desc->coeff) std::memcpy(coeff.data(), desc->coeff, sizeof(double) * K * M);

@@ -31,7 +31,7 @@ struct SerRef {
 // tid = 0..T-1 (a whole CTA, or one warp with T = 32).  get(bi, a, b, c)
 // returns the operands of convolution bi; outputs are compact series (limb
 // stride d).  T must be a multiple of 32 or equal to 32.
-template <int K, typename Get>
+template <int K, typename Get, bool CG = false>
 __device__ void conv_batch(int tid, int T, int B, int d, Get get) {
   const int P = (d + 1) / 2;
   const int groups = B * P;
@@ -54,8 +54,8 @@ __device__ void conv_batch(int tid, int T, int B, int d, Get get) {
       const bool first = t <= k1;
       const int k = first ? k1 : k2;
       const int j = first ? t : t - k1 - 1;
-      md::mdv<K> x = md::load<K>(a.p, a.ls, j);
-      md::mdv<K> y = md::load<K>(b.p, b.ls, k - j);
+      md::mdv<K> x = CG ? md::load_cg<K>(a.p, a.ls, j) : md::load<K>(a.p, a.ls, j);
+      md::mdv<K> y = CG ? md::load_cg<K>(b.p, b.ls, k - j) : md::load<K>(b.p, b.ls, k - j);
       md::mdv<K> cur;
 #pragma unroll
       for (int l = 0; l < K; ++l) cur.x[l] = first ? acc1.x[l] : acc2.x[l];
@@ -77,32 +77,126 @@ __device__ void conv_batch(int tid, int T, int B, int d, Get get) {
   }
 }
 
-// Per-CTA workspace: F[m_max], G[m_max], X[m_max] compact series (K*d doubles each)
+// ------------------------------------------------------------------ job-queue eval/diff
+// Jobs (int4 {type, a, b, c}), popped in order by persistent CTAs:
+//   JF  {0, tau}      forward chain f_1..f_{m-1} of monomial tau, publishes fprog[tau]
+//   JG  {1, tau}      backward chain g_1..g_{m-2}, publishes gprog[tau]
+//   JX  {2, tau, j}   cross product d/dx_{vj} = f_{j-2} * g_{m-j-1} (j = 2..m-1, 1-based)
+//   JE  {3, i}        equation i: b_i = r_i - sum c value, A row, dense A0 row, in
+//                     ascending monomial order (waits until its monomials are done)
+// Every chain job precedes every cross job, which precede every equation job,
+// so a job only ever waits for jobs popped earlier by resident CTAs: no
+// deadlock.  Chains are ordered longest first (LPT), cross products by the
+// layer at which their inputs appear.  Series live in a pool: F, G, X of
+// monomial tau start at ser_off[tau] (compact [K][d] series, limb stride d).
+struct EdJobs {
+  const int4* jobs;
+  int njobs;
+  const long long* ser_off;  // [M] series index of f_1 of tau; g_1 at +m-1; d/dx_2 at +2m-3
+  double* pool;
+  int* fprog;                // [M] forward products done
+  int* gprog;                // [M] backward products done
+  int* left;                 // [M] chain + cross jobs not yet finished
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_geq(const int* p, int v) {
+  int ns = 32;
+  while (ld_acquire(p) < v) {
+    __nanosleep(ns);
+    ns = min(ns * 2, 1024);
+  }
+}
+__device__ __forceinline__ void publish(int* p, int v) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <int K>
-__global__ void __launch_bounds__(256) evaldiff_kernel(DevSys s, const double* __restrict__ x,
-                                                       double* __restrict__ b, double* __restrict__ A,
-                                                       double* __restrict__ A0, double* __restrict__ ws,
-                                                       int* job_counter) {
+__global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, const double* __restrict__ x,
+                                                            double* __restrict__ b, double* __restrict__ A,
+                                                            double* __restrict__ A0, int* job_counter) {
   const int n = s.n, d = s.d, nnz = s.nnz;
   const long long ser = (long long)K * d;
-  double* F = ws + (long long)blockIdx.x * 3 * s.m_max * ser;
-  double* Gs = F + s.m_max * ser;
-  double* X = Gs + s.m_max * ser;
-  __shared__ SerRef sa[64], sb[64];
-  __shared__ double* sc[64];
-  __shared__ int s_job;
-  extern __shared__ double bacc[];  // [K][d]
-
   const long long xs = (long long)n * d;  // limb stride of x
+  __shared__ int4 s_job;
+  extern __shared__ double bacc[];  // [K][d]
   for (;;) {
-    if (threadIdx.x == 0) s_job = atomicAdd(job_counter, 1);
+    if (threadIdx.x == 0) {
+      const int id = atomicAdd(job_counter, 1);
+      s_job = (id < J.njobs) ? J.jobs[id] : make_int4(-1, 0, 0, 0);
+    }
     __syncthreads();
-    const int job = s_job;
+    const int4 jb = s_job;
     __syncthreads();
-    if (job >= n) break;
-    const int i = s.job_order[job];
+    if (jb.x < 0) break;
+    if (jb.x <= 2) {
+      const int tau = jb.y;
+      const int m0 = s.mono_ptr[tau];
+      const int m = s.mono_ptr[tau + 1] - m0;
+      const int* vars = s.var_idx + m0;
+      double* F = J.pool + J.ser_off[tau] * ser;  // F[q-1] = f_q
+      double* G = F + (m - 1) * ser;              // G[q-1] = g_q
+      double* X = G + (m - 2) * ser;              // X[j-2] = d/dx_j
+      if (jb.x == 0) {
+        for (int q = 1; q <= m - 1; ++q) {
+          auto get = [&](int, SerRef& pa, SerRef& pb, double*& pc) {
+            pa = (q == 1) ? SerRef{x + (long long)vars[0] * d, xs} : SerRef{F + (q - 2) * ser, d};
+            pb = SerRef{x + (long long)vars[q] * d, xs};
+            pc = F + (q - 1) * ser;
+          };
+          conv_batch<K, decltype(get), true>(threadIdx.x, blockDim.x, 1, d, get);
+          __syncthreads();
+          if (threadIdx.x == 0) publish(J.fprog + tau, q);
+        }
+      } else if (jb.x == 1) {
+        for (int q = 1; q <= m - 2; ++q) {
+          auto get = [&](int, SerRef& pa, SerRef& pb, double*& pc) {
+            pa = (q == 1) ? SerRef{x + (long long)vars[m - 1] * d, xs} : SerRef{G + (q - 2) * ser, d};
+            pb = SerRef{x + (long long)vars[m - 1 - q] * d, xs};
+            pc = G + (q - 1) * ser;
+          };
+          conv_batch<K, decltype(get), true>(threadIdx.x, blockDim.x, 1, d, get);
+          __syncthreads();
+          if (threadIdx.x == 0) publish(J.gprog + tau, q);
+        }
+      } else {
+        const int j = jb.z;  // 2..m-1
+        if (threadIdx.x == 0) {
+          if (j - 2 >= 1) wait_geq(J.fprog + tau, j - 2);
+          if (m - j - 1 >= 1) wait_geq(J.gprog + tau, m - j - 1);
+        }
+        __syncthreads();
+        auto get = [&](int, SerRef& pa, SerRef& pb, double*& pc) {
+          pa = (j - 2 == 0) ? SerRef{x + (long long)vars[0] * d, xs} : SerRef{F + (j - 3) * ser, d};
+          const int gq = m - j - 1;
+          pb = (gq == 0) ? SerRef{x + (long long)vars[m - 1] * d, xs} : SerRef{G + (gq - 1) * ser, d};
+          pc = X + (j - 2) * ser;
+        };
+        conv_batch<K, decltype(get), true>(threadIdx.x, blockDim.x, 1, d, get);
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicSub(J.left + tau, 1);
+      }
+      continue;
+    }
+    // ---- JE: equation i
+    const int i = jb.y;
     const int r0 = s.row_ptr[i], r1 = s.row_ptr[i + 1];
-    // b accumulator starts at r_i(t); zero the structural row of A
+    if (threadIdx.x == 0)
+      for (int tau = s.eq_ptr[i]; tau < s.eq_ptr[i + 1]; ++tau) {
+        int ns = 32;
+        while (ld_acquire(J.left + tau) > 0) {
+          __nanosleep(ns);
+          ns = min(ns * 2, 1024);
+        }
+      }
     for (int t = threadIdx.x; t < K * d; t += blockDim.x) {
       const int l = t / d, k = t % d;
       bacc[l * d + k] = s.rhs[(long long)l * xs + (long long)i * d + k];
@@ -118,81 +212,32 @@ __global__ void __launch_bounds__(256) evaldiff_kernel(DevSys s, const double* _
       const int m = s.mono_ptr[tau + 1] - m0;
       const int* vars = s.var_idx + m0;
       const int* dst = s.mono_dst + m0;
+      const double* F = J.pool + J.ser_off[tau] * ser;
+      const double* G = F + (m - 1) * ser;
+      const double* X = G + (m - 2) * ser;
       md::mdv<K> c;
 #pragma unroll
       for (int l = 0; l < K; ++l) c.x[l] = s.coeff[(long long)l * s.M + tau];
-      // ---- forward / backward chains (layers) and cross products
-      if (m >= 2) {
-        for (int q = 1; q <= m - 1; ++q) {
-          if (threadIdx.x == 0) {
-            int nb = 0;
-            sa[nb] = (q == 1) ? SerRef{x + (long long)vars[0] * d, xs} : SerRef{F + (q - 1) * ser, d};
-            sb[nb] = SerRef{x + (long long)vars[q] * d, xs};
-            sc[nb] = F + q * ser;
-            ++nb;
-            if (q <= m - 2) {
-              sa[nb] = (q == 1) ? SerRef{x + (long long)vars[m - 1] * d, xs} : SerRef{Gs + (q - 1) * ser, d};
-              sb[nb] = SerRef{x + (long long)vars[m - 1 - q] * d, xs};
-              sc[nb] = Gs + q * ser;
-              ++nb;
-            }
-            s_job = nb;
-          }
-          __syncthreads();
-          const int nb = s_job;
-          conv_batch<K>(threadIdx.x, blockDim.x, nb, d, [&](int bi, SerRef& pa, SerRef& pb, double*& pc) {
-            pa = sa[bi]; pb = sb[bi]; pc = sc[bi];
-          });
-          __syncthreads();
-        }
-        // cross products d/dx_{vj}, j = 2..m-1 (1-based) -> X[j-1]
-        for (int j0 = 2; j0 <= m - 1; j0 += 64) {
-          const int cnt = min(64, m - j0);
-          if (threadIdx.x < cnt) {
-            const int j = j0 + threadIdx.x;
-            sa[threadIdx.x] = (j - 2 == 0) ? SerRef{x + (long long)vars[0] * d, xs} : SerRef{F + (j - 2) * ser, d};
-            const int gq = m - j - 1;
-            sb[threadIdx.x] = (gq == 0) ? SerRef{x + (long long)vars[m - 1] * d, xs} : SerRef{Gs + gq * ser, d};
-            sc[threadIdx.x] = X + (j - 1) * ser;
-          }
-          __syncthreads();
-          conv_batch<K>(threadIdx.x, blockDim.x, cnt, d, [&](int bi, SerRef& pa, SerRef& pb, double*& pc) {
-            pa = sa[bi]; pb = sb[bi]; pc = sc[bi];
-          });
-          __syncthreads();
-        }
-      }
-      // ---- b_i -= c * value ; A[i][v_q] += c * d/dx_{v_q}
       for (int k = threadIdx.x; k < d; k += blockDim.x) {
-        md::mdv<K> val;
-        if (m == 1) val = md::load<K>(x + (long long)vars[0] * d, xs, k);
-        else val = md::load<K>(F + (m - 1) * ser, d, k);
+        md::mdv<K> val = (m == 1) ? md::load<K>(x + (long long)vars[0] * d, xs, k)
+                                  : md::load_cg<K>(F + (m - 2) * ser, d, k);
         md::mdv<K> acc = md::load<K>(bacc, d, k);
-        acc = md::fma_acc<K>(acc, md::neg<K>(c), val);
-        md::store<K>(bacc, d, k, acc);
+        md::store<K>(bacc, d, k, md::fma_acc<K>(acc, md::neg<K>(c), val));
       }
       for (int t = threadIdx.x; t < m * d; t += blockDim.x) {
         const int q = t % m, k = t / m;
         md::mdv<K> part;
-        if (m == 1) {
-          part = md::from_double<K>(k == 0 ? 1.0 : 0.0);
-        } else if (m == 2) {
-          part = md::load<K>(x + (long long)vars[1 - q] * d, xs, k);
-        } else if (q == 0) {
-          part = md::load<K>(Gs + (m - 2) * ser, d, k);
-        } else if (q == m - 1) {
-          part = md::load<K>(F + (m - 2) * ser, d, k);
-        } else {
-          part = md::load<K>(X + q * ser, d, k);
-        }
+        if (m == 1) part = md::from_double<K>(k == 0 ? 1.0 : 0.0);
+        else if (m == 2) part = md::load<K>(x + (long long)vars[1 - q] * d, xs, k);
+        else if (q == 0) part = md::load_cg<K>(G + (m - 3) * ser, d, k);        // g_{m-2}
+        else if (q == m - 1) part = md::load_cg<K>(F + (m - 3) * ser, d, k);    // f_{m-2}
+        else part = md::load_cg<K>(X + (q - 1) * ser, d, k);                    // d/dx_{q+1}
         const long long e = dst[q];
         md::mdv<K> acc = md::load<K>(A + (long long)k * nnz, (long long)d * nnz, e);
-        acc = md::fma_acc<K>(acc, c, part);
-        md::store<K>(A + (long long)k * nnz, (long long)d * nnz, e, acc);
+        md::store<K>(A + (long long)k * nnz, (long long)d * nnz, e, md::fma_acc<K>(acc, c, part));
       }
       __syncthreads();
     }
-    // ---- write b column i and the dense row i of A0
     for (int t = threadIdx.x; t < K * d; t += blockDim.x) {
       const int l = t / d, k = t % d;
       b[((long long)l * d + k) * n + i] = bacc[l * d + k];

@@ -17,10 +17,12 @@ namespace {
 template <int K>
 ns_status launch_evaldiff(ns_system* s, const double* x, cudaStream_t st) {
   CK(cudaMemsetAsync(s->job_counter, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(s->prog, 0, sizeof(int) * 2 * s->M, st));
+  CK(cudaMemcpyAsync(s->left, s->left_init, sizeof(int) * s->M, cudaMemcpyDeviceToDevice, st));
   DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
             s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
-  ns::evaldiff_kernel<K><<<s->grid_ed, 256, s->ed_smem, st>>>(ds, x, s->b, s->A, s->A0, s->ws,
-                                                              s->job_counter);
+  ns::EdJobs J{s->jobs, s->njobs, s->ser_off, s->pool, s->prog, s->prog + s->M, s->left};
+  ns::evaldiff_jobs_kernel<K><<<s->grid_ed, 256, s->ed_smem, st>>>(ds, J, x, s->b, s->A, s->A0, s->job_counter);
   s->last_launches += 1;
   CK(cudaGetLastError());
   return NS_OK;
@@ -86,9 +88,10 @@ ns_status setup_grids(ns_system* s) {
   s->grid_st = s->sms;
   if (const char* e = getenv("NS_STAGE_GRID")) s->grid_st = std::max(1, std::min(s->sms * occ, atoi(e)));
   s->ed_smem = sizeof(double) * (size_t)K * s->d;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::evaldiff_kernel<K>, 256, s->ed_smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::evaldiff_jobs_kernel<K>, 256, s->ed_smem));
   if (occ < 1) return NS_ECUDA;
-  s->grid_ed = std::min(s->n, occ * s->sms);
+  s->grid_ed = std::min(s->njobs, occ * s->sms);
+  if (const char* e = getenv("NS_ED_GRID")) s->grid_ed = std::max(1, std::min(occ * s->sms, atoi(e)));
   return NS_OK;
 }
 

@@ -24,6 +24,14 @@ struct ns_system {
   int cmax = 1;
   double *y = nullptr, *rbuf = nullptr, *knorm = nullptr, *res_tmp = nullptr, *ws = nullptr;
   int* job_counter = nullptr;
+  // eval/diff job queue (evaldiff.cuh): jobs, series pool, progress counters
+  int4* jobs = nullptr;
+  int njobs = 0;
+  long long* ser_off = nullptr;
+  double* pool = nullptr;
+  int* prog = nullptr;       // [2M]: fprog, gprog
+  int* left = nullptr;       // [M]
+  int* left_init = nullptr;  // [M]
   unsigned* bar = nullptr;     // [4]: qr barrier, stage barrier
   unsigned* status = nullptr;  // device status word
   int grid_ed = 0, grid_qr = 0, grid_st = 0;
