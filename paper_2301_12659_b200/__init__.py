@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(_HERE, "libnewtonmd.so")
 NS_REUSE_QR = 1
 NS_NO_RESIDUAL = 2
 NS_LEDGER = 4
+NS_TILED_BS = 8
 
 STATUS = {0: "NS_OK", 1: "NS_EINVAL", 2: "NS_EPREC", 3: "NS_EDIM", 4: "NS_EMONO", 5: "NS_ESINGULAR",
           6: "NS_ENONFINITE", 7: "NS_ENOMEM", 8: "NS_ECUDA", 9: "NS_ENCCL", 10: "NS_ESTATE"}

@@ -91,7 +91,7 @@ ns_status collect_ledger(ns_system* s) {
 void free_all(ns_system* s) {
   void* ptrs[] = {s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst, s->row_ptr, s->col_idx, s->job_order,
                   s->coeff, s->rhs, s->b, s->A, s->A0, s->W, s->vhead, s->beta, s->rdiag, s->R, s->Qt,
-                  s->invR, s->bp, s->dx, s->y, s->part, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
+                  s->invR, s->bp, s->dx, s->y, s->part, s->Minv, s->Z, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
                   s->bar, s->status, s->bws, s->jobs, s->ser_off, s->pool, s->prog, s->left,
                   s->left_init};
   for (void* p : ptrs)
@@ -253,6 +253,8 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->bp, (size_t)K * d * n) == cudaSuccess;
   ok &= dalloc(&s->dx, (size_t)K * d * n) == cudaSuccess;
   ok &= dalloc(&s->y, (size_t)K * n) == cudaSuccess;
+  ok &= dalloc(&s->Minv, (size_t)K * nn) == cudaSuccess;
+  ok &= dalloc(&s->Z, (size_t)K * nn) == cudaSuccess;
   {
     int maxlen = 1;
     for (int i = 0; i < n; ++i) maxlen = std::max(maxlen, s->h_row_ptr[i + 1] - s->h_row_ptr[i]);
@@ -263,7 +265,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->knorm, (size_t)3 * K * d) == cudaSuccess;
   ok &= dalloc(&s->res_tmp, (size_t)K * 3) == cudaSuccess;
   ok &= dalloc(&s->job_counter, 1) == cudaSuccess;
-  ok &= dalloc(&s->bar, 4) == cudaSuccess;
+  ok &= dalloc(&s->bar, 8) == cudaSuccess;
   ok &= dalloc(&s->status, 1) == cudaSuccess;
   if (!ok) return fail(NS_ENOMEM);
   switch (K) {
@@ -300,7 +302,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= cudaMemcpy(s->coeff, coeff.data(), sizeof(double) * K * M, cudaMemcpyHostToDevice) == cudaSuccess;
   ok &= cudaMemcpy(s->rhs, desc->rhs, sizeof(double) * K * n * d, cudaMemcpyHostToDevice) == cudaSuccess;
   ok &= cudaMemset(s->status, 0, sizeof(unsigned)) == cudaSuccess;
-  ok &= cudaMemset(s->bar, 0, 4 * sizeof(unsigned)) == cudaSuccess;
+  ok &= cudaMemset(s->bar, 0, 8 * sizeof(unsigned)) == cudaSuccess;
   for (auto& row : s->ev)
     for (auto& e : row) ok &= cudaEventCreate(&e) == cudaSuccess;
   if (!ok) return fail(NS_ECUDA);
@@ -321,8 +323,10 @@ ns_status ns_newton_series_step(ns_system* s, int precision, int dim, int degree
   if (!s || !x) return NS_EINVAL;
   if (precision != s->K) return NS_EPREC;
   if (dim != s->n || degree != s->D) return NS_EDIM;
-  if (flags & ~(NS_REUSE_QR | NS_NO_RESIDUAL | NS_LEDGER)) return NS_EINVAL;
+  if (flags & ~(NS_REUSE_QR | NS_NO_RESIDUAL | NS_LEDGER | NS_TILED_BS)) return NS_EINVAL;
   if ((flags & NS_REUSE_QR) && !s->qr_cached) return NS_ESTATE;
+  if ((flags & NS_REUSE_QR) && !(flags & NS_TILED_BS) && !s->use_m) return NS_ESTATE;  // cached without M
+  if (!(flags & NS_REUSE_QR)) s->use_m = !(flags & NS_TILED_BS);
   cudaStream_t st = (cudaStream_t)stream;
   switch (s->K) {
     case 2: return step_impl<2>(s, x, res_out, flags, st);

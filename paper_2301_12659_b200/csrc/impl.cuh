@@ -41,8 +41,19 @@ ns_status launch_qr(ns_system* s, cudaStream_t st) {
   const long long tot = (long long)K * n * n;
   const int blocks = (int)std::min<long long>((tot + 255) / 256, 4LL * s->sms);
   ns::qr_unpack_kernel<K><<<blocks, 256, 0, st>>>(n, s->W, s->R, s->Qt);
-  ns::invert_tiles_kernel<K><<<s->T, 256, 0, st>>>(n, s->TB, s->R, s->invR);
+  const size_t inv_smem = sizeof(double) * (size_t)K * (2 * s->TB * s->TB + s->TB * s->TB / 2);
+  ns::invert_tiles_kernel<K><<<s->T, 256, inv_smem, st>>>(n, s->TB, s->R, s->invR);
   s->last_launches += 3;
+  if (s->use_m) {
+    CK(cudaMemsetAsync(s->bar + 4, 0, 2 * sizeof(unsigned), st));
+    int TB = s->TB;
+    const double *R = s->R, *Qt = s->Qt, *iR = s->invR;
+    double *M = s->Minv, *Z = s->Z;
+    unsigned* bar2 = s->bar + 4;
+    void* margs[] = {&n, &TB, (void*)&R, (void*)&Qt, (void*)&iR, &M, &Z, &bar2};
+    CK(cudaLaunchCooperativeKernel((const void*)ns::form_m_kernel<K>, dim3(s->grid_st), dim3(128), margs, 0, st));
+    s->last_launches += 1;
+  }
   CK(cudaGetLastError());
   s->qr_cached = true;
   return NS_OK;
@@ -54,7 +65,8 @@ ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
   CK(cudaMemsetAsync(s->dx, 0, sizeof(double) * (size_t)K * s->d * s->n, st));
   DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
             s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
-  ns::StageArgs a{s->b, s->A, s->Qt, s->R, s->invR, s->bp, s->dx, s->y, s->part, s->cmax, s->TB, k_lo};
+  ns::StageArgs a{s->b, s->A, s->Qt, s->R, s->invR, s->bp, s->dx, s->y, s->part, s->use_m ? s->Minv : nullptr,
+                  s->cmax, s->TB, k_lo};
   unsigned* bar = s->bar + 2;
   void* args[] = {&ds, &a, &bar};
   CK(cudaLaunchCooperativeKernel((const void*)ns::stage_kernel<K>, dim3(s->grid_st), dim3(128), args, 0, st));
@@ -86,6 +98,10 @@ ns_status setup_grids(ns_system* s) {
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::stage_kernel<K>, 128, 0));
   if (occ < 1) return NS_ECUDA;
   s->grid_st = s->sms;
+  {
+    const size_t inv_smem = sizeof(double) * (size_t)K * (2 * s->TB * s->TB + s->TB * s->TB / 2);
+    CK(cudaFuncSetAttribute(ns::invert_tiles_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inv_smem));
+  }
   if (const char* e = getenv("NS_STAGE_GRID")) s->grid_st = std::max(1, std::min(s->sms * occ, atoi(e)));
   s->ed_smem = sizeof(double) * (size_t)K * s->d;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::evaldiff_jobs_kernel<K>, 256, s->ed_smem));

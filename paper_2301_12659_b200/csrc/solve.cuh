@@ -145,46 +145,111 @@ __global__ void qr_unpack_kernel(int n, const double* __restrict__ W, double* R,
   }
 }
 
-// inverse of the diagonal tile t of R (size nb <= 32): one warp per column of
-// the inverse; X[r][c] = -(sum_{q=r+1}^{c} R[r][q] X[q][c]) / R[r][r].
-// invR layout: [K][T][32][32] row-major per tile.
+// Inverse of the diagonal tile t of R (size nb <= TB = 32) by recursive
+// doubling: inv([[A, B], [0, C]]) = [[inv A, -inv A B inv C], [0, inv C]],
+// levels s = 2, 4, ..., 32; each level is two small products whose entries
+// are independent (one thread each), so the dependent chain is
+// 2 (1 + 2 + 4 + 8 + 16) = 62 md multiply-adds instead of 32 x (dot + butterfly).
+// Rows/columns >= nb are padded with the identity.  invR: [K][T][TB][TB] row-major.
 template <int K>
 __global__ void __launch_bounds__(256) invert_tiles_kernel(int n, int TB, const double* __restrict__ R,
                                                            double* invR) {
+  extern __shared__ double sm[];
   const int t = blockIdx.x;
   const int t0 = t * TB;
   const int nb = min(TB, n - t0);
-  const int lane = lane_id();
   const int T = (n + TB - 1) / TB;
   const long long lsR = (long long)n * n;
   const long long lsI = (long long)T * TB * TB;
-  // 1 / R_qq for q = lane
-  md::mdv<K> inv_d = md::zero<K>();
-  if (lane < nb) {
-    md::mdv<K> rqq = md::load<K>(R, lsR, (long long)(t0 + lane) * n + t0 + lane);
-    inv_d = md::recip<K>(rqq);
+  const int TT = TB * TB;
+  double* sR = sm;                 // [K][TB][TB]
+  double* sX = sm + (long long)K * TT;  // [K][TB][TB]
+  double* sT = sX + (long long)K * TT;  // [K][TT/2] level scratch
+  for (int e = threadIdx.x; e < TT; e += blockDim.x) {
+    const int r = e / TB, c = e % TB;
+    md::mdv<K> v = md::zero<K>();
+    if (r < nb && c < nb) {
+      if (c >= r) v = md::load<K>(R, lsR, (long long)(t0 + r) * n + t0 + c);
+    } else if (r == c) {
+      v = md::from_double<K>(1.0);
+    }
+    md::store<K>(sR, TT, e, v);
+    md::store<K>(sX, TT, e, md::zero<K>());
   }
-  for (int c = threadIdx.x >> 5; c < TB; c += blockDim.x >> 5) {  // column of the inverse
-    md::mdv<K> X = md::zero<K>();  // lane q holds X[q][c]
-    if (c < nb) {
-      if (lane == c) X = inv_d;
-      for (int r = c - 1; r >= 0; --r) {
-        md::mdv<K> p = md::zero<K>();
-        if (lane > r && lane <= c) {
-          md::mdv<K> rr = md::load<K>(R, lsR, (long long)(t0 + r) * n + t0 + lane);
-          p = md::mul<K>(rr, X);
-        }
-        p = md::group_sum<K>(p, 32);
-        md::mdv<K> idr = md::shfl<K>(inv_d, r);
-        md::mdv<K> xr = md::neg<K>(md::mul<K>(p, idr));
-        if (lane == r) X = xr;
+  __syncthreads();
+  for (int r = threadIdx.x; r < TB; r += blockDim.x)
+    md::store<K>(sX, TT, r * TB + r, md::recip<K>(md::load<K>(sR, TT, r * TB + r)));
+  __syncthreads();
+  for (int sz = 2; sz <= TB; sz <<= 1) {
+    const int h = sz >> 1;
+    const int nent = (TB / sz) * h * h;
+    // T1[blk][p][q] = sum_{u=0}^{q} R[base+p][base+h+u] X[base+h+u][base+h+q]
+    for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+      const int blk = e / (h * h), p = (e / h) % h, q = e % h;
+      const int base = blk * sz;
+      md::mdv<K> acc = md::zero<K>();
+      for (int u = 0; u <= q; ++u)
+        acc = md::fma_acc<K>(acc, md::load<K>(sR, TT, (base + p) * TB + base + h + u),
+                             md::load<K>(sX, TT, (base + h + u) * TB + base + h + q));
+      md::store<K>(sT, TT / 2, e, acc);
+    }
+    __syncthreads();
+    // X[base+p][base+h+q] = - sum_{v=p}^{h-1} X[base+p][base+v] T1[blk][v][q]
+    for (int e = threadIdx.x; e < nent; e += blockDim.x) {
+      const int blk = e / (h * h), p = (e / h) % h, q = e % h;
+      const int base = blk * sz;
+      md::mdv<K> acc = md::zero<K>();
+      for (int v = p; v < h; ++v)
+        acc = md::fma_acc<K>(acc, md::load<K>(sX, TT, (base + p) * TB + base + v),
+                             md::load<K>(sT, TT / 2, blk * h * h + v * h + q));
+      md::store<K>(sX, TT, (base + p) * TB + base + h + q, md::neg<K>(acc));
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < TT; e += blockDim.x) {
+    const int r = e / TB, c = e % TB;
+    md::mdv<K> v = (r < nb && c < nb) ? md::load<K>(sX, TT, e) : md::zero<K>();
+    md::store<K>(invR, lsI, (long long)t * TT + e, v);
+  }
+}
+
+// M = R^{-1} Q^T (row-major [K][n][n]) by tiled back substitution on the n
+// columns of Q^T, tiles last to first:  Z_t = Q^T_t - sum_{c >= t1} R[t][c] M[c],
+// M_t = invR_t Z_t.  One lane per column j, serial over c (once per QR).
+// With M each stage's "Q^T b then back substitution" is one matvec
+// dx_k = M b'_k (same algebra, R^{-1}(Q^T b) = (R^{-1} Q^T) b).
+template <int K>
+__global__ void __launch_bounds__(128) form_m_kernel(int n, int TB, const double* __restrict__ R,
+                                                     const double* __restrict__ Qt, const double* __restrict__ invR,
+                                                     double* M, double* Z, unsigned* bar) {
+  const int gw = gwarp(), nw = nwarps(), lane = lane_id();
+  const int T = (n + TB - 1) / TB;
+  const long long lsM = (long long)n * n, lsI = (long long)T * TB * TB;
+  const int jg = (n + 31) / 32;  // 32-column groups
+  for (int t = T - 1; t >= 0; --t) {
+    const int t0 = t * TB, t1 = min(n, t0 + TB);
+    for (int w = gw; w < (t1 - t0) * jg; w += nw) {
+      const int r = t0 + w / jg, j = (w % jg) * 32 + lane;
+      if (j < n) {
+        md::mdv<K> acc = md::load<K>(Qt, lsM, (long long)r * n + j);
+        for (int c = t1; c < n; ++c)
+          acc = md::fma_acc<K>(acc, md::neg<K>(md::load<K>(R, lsM, (long long)r * n + c)),
+                               md::load_cg<K>(M, lsM, (long long)c * n + j));
+        md::store_cg<K>(Z, lsM, (long long)r * n + j, acc);
       }
     }
-    // store column c of the tile inverse (zeros outside nb)
-    if (lane < TB) {
-      md::mdv<K> v = (lane < nb && c < nb && lane <= c) ? X : md::zero<K>();
-      md::store<K>(invR, lsI, (long long)t * TB * TB + (long long)lane * TB + c, v);
+    grid_sync(bar);
+    for (int w = gw; w < (t1 - t0) * jg; w += nw) {
+      const int r = t0 + w / jg, j = (w % jg) * 32 + lane;
+      if (j < n) {
+        md::mdv<K> acc = md::zero<K>();
+        for (int c = t0; c < t1; ++c)
+          acc = md::fma_acc<K>(acc, md::load<K>(invR, lsI, (long long)t * TB * TB + (long long)(r - t0) * TB + (c - t0)),
+                               md::load_cg<K>(Z, lsM, (long long)c * n + j));
+        md::store_cg<K>(M, lsM, (long long)r * n + j, acc);
+      }
     }
+    grid_sync(bar);
   }
 }
 
@@ -199,6 +264,7 @@ struct StageArgs {
   double* dx;          // [K][d][n]
   double* y;           // [K][n]
   double* part;        // [K][n][cmax] partial sums of the update chunks
+  const double* M;     // [K][n][n] = R^{-1} Q^T, or nullptr for the per-stage tiled path
   int cmax;            // max chunks per row = ceil((d-1) * maxlen / UCH)
   int TB;
   int k_lo;
@@ -263,6 +329,19 @@ __global__ void __launch_bounds__(128) stage_kernel(DevSys s, StageArgs a, unsig
         if (lane == 0) md::store_cg<K>(a.bp + (long long)k * n, lsV, i, md::load<K>(a.b + (long long)k * n, lsV, i));
     }
     grid_sync(bar);
+    if (a.M) {
+      // ---- dx_k = M b'_k  (qhb and bs in one matvec)
+      for (int i = gw; i < n; i += nw) {
+        md::mdv<K> acc = md::zero<K>();
+        for (int c = lane; c < n; c += 32)
+          acc = md::fma_acc<K>(acc, md::load<K>(a.M, lsM, (long long)i * n + c),
+                               md::load_cg<K>(a.bp + (long long)k * n, lsV, c));
+        acc = md::group_sum<K>(acc, 32);
+        if (lane == 0) md::store_cg<K>(a.dx + (long long)k * n, lsV, i, acc);
+      }
+      grid_sync(bar);
+      continue;
+    }
     // ---- qhb: y = Q^T b'_k
     for (int i = gw; i < n; i += nw) {
       md::mdv<K> acc = md::zero<K>();

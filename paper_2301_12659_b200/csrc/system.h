@@ -21,6 +21,8 @@ struct ns_system {
   double *b = nullptr, *A = nullptr, *A0 = nullptr, *W = nullptr, *vhead = nullptr, *beta = nullptr;
   double *rdiag = nullptr, *R = nullptr, *Qt = nullptr, *invR = nullptr, *bp = nullptr, *dx = nullptr;
   double *part = nullptr;
+  double *Minv = nullptr, *Z = nullptr;  // M = R^{-1} Q^T and its scratch
+  bool use_m = true;                  // false: per-stage tiled back substitution (NS_TILED_BS)
   int cmax = 1;
   double *y = nullptr, *rbuf = nullptr, *knorm = nullptr, *res_tmp = nullptr, *ws = nullptr;
   int* job_counter = nullptr;

@@ -314,3 +314,23 @@ def test_C3_sampled_parity():
                 for e in range(rp[i], rp[i + 1]):
                     r -= H.limbs_to_fraction(g["A"][:, j, e]) * H.limbs_to_fraction(g["dx"][:, k - j, ci[e]])
             assert abs(r) <= Fraction(tol) * scale_k, (i, k, float(abs(r) / scale_k))
+
+
+@pytest.mark.parametrize("K,n,D", [(4, 36, 20), (8, 40, 12)])
+def test_tiled_back_substitution_mode(K, n, D):
+    """NS_TILED_BS: per stage y = Q^T b'_k then tiled back substitution (P:659-663,
+    P:124-126) instead of dx_k = M b'_k; both must meet the tolerance."""
+    import paper_2301_12659_b200 as P
+    torch = _torch()
+    sys_ = synth.triangular_system(n, D, K, seed=31)
+    x_np = synth.make_x(sys_, "near", seed=32)
+    F = O.field_for(K)
+    out = H.step_oracle(sys_, x_np, F)
+    sc = O.scales(sys_, x_np)
+    dxf = np.array([[float(out["dx"][k][i]) for i in range(n)] for k in range(D + 1)])
+    s_k, _ = O.stage_scales(sys_, x_np, H.dense_A0_float(out["A"], n), dxf, sc["s_b"], sc["s_A"])
+    for flags in (P.NS_TILED_BS, 0):
+        h = _handle(sys_)
+        x = torch.tensor(x_np, device="cuda:0")
+        h.step(x, flags=flags)
+        assert H.xnew_errors(sys_, x_np, out, _np(x), F, s_k) <= 1, flags
