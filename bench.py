@@ -317,6 +317,8 @@ def run_ours(args):
         "peak_derived_gflops": peaks["gflops"],
         "fp64_pipe_frac": PM.instr(per_class[dom], sys_.K) / (dom_ms * 1e-3) * 1e-9 / probe["ginstr_per_s"],
         "class_ms_per_step": {k: v / max(1, led["steps"]) for k, v in cls_ms.items()},
+        "ledger_step_ms": led["ms_total"] / max(1, led["steps"]),
+        "note": "eval/diff runs on a side stream concurrently with A0 + QR; class times overlap",
     }
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps,

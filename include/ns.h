@@ -87,10 +87,11 @@ typedef struct {
 /* kernel classes of T4; updates, qhb and bs are fused into one
  * persistent stage kernel and reported together as "stage" */
 typedef struct {
-  double ms_convolution; /* eval/diff                                   */
-  double ms_qr;          /* Householder QR + unpack + tile inversion     */
-  double ms_stage;       /* updates + Q^T b + back substitution           */
-  double ms_residual;    /* residuals + x update + norms                 */
+  double ms_convolution; /* eval/diff (side stream, concurrent with the QR) */
+  double ms_qr;          /* A_0 + Householder QR + tile inverses + M       */
+  double ms_stage;       /* updates + Q^T b + back substitution            */
+  double ms_residual;    /* residuals + x update + norms                  */
+  double ms_total;       /* whole step (start to end, the overlap included) */
   int64_t steps;         /* ledger steps accumulated                     */
   int64_t qr_count;      /* QR factorisations performed                  */
 } ns_ledger;

@@ -54,7 +54,7 @@ class StepInfo(ctypes.Structure):
 
 class Ledger(ctypes.Structure):
     _fields_ = [("ms_convolution", ctypes.c_double), ("ms_qr", ctypes.c_double),
-                ("ms_stage", ctypes.c_double), ("ms_residual", ctypes.c_double),
+                ("ms_stage", ctypes.c_double), ("ms_residual", ctypes.c_double), ("ms_total", ctypes.c_double),
                 ("steps", ctypes.c_int64), ("qr_count", ctypes.c_int64)]
 
     def as_dict(self):

@@ -32,6 +32,10 @@ ns_status collect_one(ns_system* s);
 
 template <int K>
 ns_status step_impl(ns_system* s, double* x, double* res_out, uint32_t flags, cudaStream_t st) {
+  // Fork: eval/diff on the side stream; on the caller's stream A_0 alone
+  // (a0_kernel) then the QR of A_0, concurrently.  Join before the stage loop.
+  // Ledger events: e0 start | e1 end eval/diff (side) | e2 end QR | e3 join |
+  // e4 end stage loop | e5 end residual.
   const bool ledger = (flags & NS_LEDGER) != 0;
   s->last_launches = 0;
   cudaEvent_t* ev = nullptr;
@@ -43,21 +47,31 @@ ns_status step_impl(ns_system* s, double* x, double* res_out, uint32_t flags, cu
     ev = s->ev[(s->ledger_head + s->ledger_count) % ns_system::LRING];
     CK(cudaEventRecord(ev[0], st));
   }
-  ns_status r = Impl<K>::evaldiff(s, x, st);
-  if (r) return r;
-  if (ledger) CK(cudaEventRecord(ev[1], st));
+  CK(cudaEventRecord(s->ev_fork, st));
+  CK(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+  ns_status r;
   if (!(flags & NS_REUSE_QR)) {
-    r = Impl<K>::qr(s, st);
+    r = Impl<K>::a0(s, x, st);
+    if (r) return r;
+  }
+  r = Impl<K>::evaldiff(s, x, s->side);
+  if (r) return r;
+  if (ledger) CK(cudaEventRecord(ev[1], s->side));
+  CK(cudaEventRecord(s->ev_join, s->side));
+  if (!(flags & NS_REUSE_QR)) {
+    r = Impl<K>::qr(s, s->A0q, st);
     if (r) return r;
   }
   if (ledger) CK(cudaEventRecord(ev[2], st));
+  CK(cudaStreamWaitEvent(st, s->ev_join, 0));
+  if (ledger) CK(cudaEventRecord(ev[3], st));
   r = Impl<K>::stage(s, 0, st);
   if (r) return r;
-  if (ledger) CK(cudaEventRecord(ev[3], st));
+  if (ledger) CK(cudaEventRecord(ev[4], st));
   r = Impl<K>::residual(s, x, res_out, st);
   if (r) return r;
   if (ledger) {
-    CK(cudaEventRecord(ev[4], st));
+    CK(cudaEventRecord(ev[5], st));
     s->ledger_count += 1;
     if (!(flags & NS_REUSE_QR)) s->ledger.qr_count += 1;
   }
@@ -67,13 +81,18 @@ ns_status step_impl(ns_system* s, double* x, double* res_out, uint32_t flags, cu
 
 ns_status collect_one(ns_system* s) {
   cudaEvent_t* ev = s->ev[s->ledger_head];
-  CK(cudaEventSynchronize(ev[4]));
-  float ms[4];
-  for (int i = 0; i < 4; ++i) CK(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
-  s->ledger.ms_convolution += ms[0];
-  s->ledger.ms_qr += ms[1];
-  s->ledger.ms_stage += ms[2];
-  s->ledger.ms_residual += ms[3];
+  CK(cudaEventSynchronize(ev[5]));
+  float conv, qr, stage, resid, total;
+  CK(cudaEventElapsedTime(&conv, ev[0], ev[1]));
+  CK(cudaEventElapsedTime(&qr, ev[0], ev[2]));
+  CK(cudaEventElapsedTime(&stage, ev[3], ev[4]));
+  CK(cudaEventElapsedTime(&resid, ev[4], ev[5]));
+  CK(cudaEventElapsedTime(&total, ev[0], ev[5]));
+  s->ledger.ms_convolution += conv;   // concurrent with the QR (side stream)
+  s->ledger.ms_qr += qr;
+  s->ledger.ms_stage += stage;
+  s->ledger.ms_residual += resid;
+  s->ledger.ms_total += total;
   s->ledger.steps += 1;
   s->ledger_head = (s->ledger_head + 1) % ns_system::LRING;
   s->ledger_count -= 1;
@@ -92,13 +111,16 @@ void free_all(ns_system* s) {
   void* ptrs[] = {s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst, s->row_ptr, s->col_idx, s->job_order,
                   s->coeff, s->rhs, s->b, s->A, s->A0, s->W, s->vhead, s->beta, s->rdiag, s->R, s->Qt,
                   s->invR, s->bp, s->dx, s->y, s->part, s->Minv, s->Z, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
-                  s->bar, s->status, s->bws, s->jobs, s->ser_off, s->pool, s->prog, s->left,
+                  s->bar, s->status, s->bws, s->A0q, s->jobs, s->ser_off, s->pool, s->prog, s->left,
                   s->left_init};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& row : s->ev)
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
+  if (s->side) cudaStreamDestroy(s->side);
 }
 
 }  // namespace
@@ -243,6 +265,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->b, (size_t)K * d * n) == cudaSuccess;
   ok &= dalloc(&s->A, (size_t)K * d * s->nnz) == cudaSuccess;
   ok &= dalloc(&s->A0, (size_t)K * nn) == cudaSuccess;
+  ok &= dalloc(&s->A0q, (size_t)K * nn) == cudaSuccess;
   ok &= dalloc(&s->W, (size_t)K * 2 * nn) == cudaSuccess;
   ok &= dalloc(&s->vhead, (size_t)K * n) == cudaSuccess;
   ok &= dalloc(&s->beta, (size_t)K * n) == cudaSuccess;
@@ -305,6 +328,9 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= cudaMemset(s->bar, 0, 8 * sizeof(unsigned)) == cudaSuccess;
   for (auto& row : s->ev)
     for (auto& e : row) ok &= cudaEventCreate(&e) == cudaSuccess;
+  ok &= cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming) == cudaSuccess;
+  ok &= cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming) == cudaSuccess;
+  ok &= cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) == cudaSuccess;
   if (!ok) return fail(NS_ECUDA);
   *out = s;
   return NS_OK;
@@ -386,13 +412,14 @@ ns_status ns_toeplitz_solve(ns_system* s, const double* b, const double* A, cons
   const size_t K = s->K, d = s->d, n = s->n;
   CK(cudaMemcpyAsync(s->b, b, sizeof(double) * K * d * n, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(s->A, A, sizeof(double) * K * d * s->nnz, cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(s->A0, A0, sizeof(double) * K * n * n, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(s->A0q, A0, sizeof(double) * K * n * n, cudaMemcpyDeviceToDevice, st));
   ns_status r;
   s->last_launches = 0;
+  s->use_m = true;
   switch (s->K) {
-    case 2: r = Impl<2>::qr(s, st); if (!r) r = Impl<2>::stage(s, 0, st); break;
-    case 4: r = Impl<4>::qr(s, st); if (!r) r = Impl<4>::stage(s, 0, st); break;
-    default: r = Impl<8>::qr(s, st); if (!r) r = Impl<8>::stage(s, 0, st); break;
+    case 2: r = Impl<2>::qr(s, s->A0q, st); if (!r) r = Impl<2>::stage(s, 0, st); break;
+    case 4: r = Impl<4>::qr(s, s->A0q, st); if (!r) r = Impl<4>::stage(s, 0, st); break;
+    default: r = Impl<8>::qr(s, s->A0q, st); if (!r) r = Impl<8>::stage(s, 0, st); break;
   }
   if (r) return r;
   CK(cudaMemcpyAsync(dx, s->dx, sizeof(double) * K * d * n, cudaMemcpyDeviceToDevice, st));

@@ -256,3 +256,65 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
 }
 
 }  // namespace ns
+
+namespace ns {
+// Dense A_0 alone (the t^0 coefficients of the Jacobian), for the QR to start
+// before the full eval/diff finishes: A_0[i][v_q] = sum_tau c_tau prod_{r != q} x_{v_r,0}.
+// One warp per equation; prefix and suffix products of the m scalars by a
+// chunked warp scan (md multiplications in a fixed order), so the dependent
+// chain is ~2 ceil(m/32) + 5 products instead of m.
+template <int K>
+__device__ md::mdv<K> warp_excl_scan_mul(md::mdv<K> v) {
+  const int lane = threadIdx.x & 31;
+  // inclusive Hillis-Steele scan, then shift by one
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    md::mdv<K> o = md::shfl<K>(v, max(lane - off, 0));
+    if (lane >= off) v = md::mul<K>(o, v);
+  }
+  md::mdv<K> e = md::shfl<K>(v, max(lane - 1, 0));
+  return lane == 0 ? md::from_double<K>(1.0) : e;
+}
+
+template <int K>
+__global__ void __launch_bounds__(128) a0_kernel(DevSys s, const double* __restrict__ x, double* __restrict__ A0q) {
+  const int n = s.n, d = s.d;
+  const long long xs = (long long)n * d, lsA = (long long)n * n;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = gw; i < n; i += nw) {
+    for (int j = lane; j < n; j += 32) md::store<K>(A0q, lsA, (long long)i * n + j, md::zero<K>());
+    __syncwarp();
+    for (int tau = s.eq_ptr[i]; tau < s.eq_ptr[i + 1]; ++tau) {
+      const int m0 = s.mono_ptr[tau], m = s.mono_ptr[tau + 1] - m0;
+      const int* vars = s.var_idx + m0;
+      md::mdv<K> c;
+#pragma unroll
+      for (int l = 0; l < K; ++l) c.x[l] = s.coeff[(long long)l * s.M + tau];
+      const int C = (m + 31) / 32;  // chunk per lane
+      const int q0 = lane * C;
+      // local exclusive prefix and suffix products inside the chunk
+      md::mdv<K> lp = md::from_double<K>(1.0), ls = md::from_double<K>(1.0);
+      for (int q = q0; q < min(m, q0 + C); ++q) lp = md::mul<K>(lp, md::load<K>(x + (long long)vars[q] * d, xs, 0));
+      for (int q = min(m, q0 + C) - 1; q >= q0; --q) ls = md::mul<K>(md::load<K>(x + (long long)vars[q] * d, xs, 0), ls);
+      // lanes' chunk products: prefix over lower lanes, suffix over higher lanes
+      md::mdv<K> pre = warp_excl_scan_mul<K>(lp);
+      // suffix scan: reverse the lane order
+      md::mdv<K> rv = md::shfl<K>(ls, 31 - lane);
+      md::mdv<K> sufr = warp_excl_scan_mul<K>(rv);
+      md::mdv<K> suf = md::shfl<K>(sufr, 31 - lane);
+      // walk the chunk: P_q = pre * prod_{q0<=r<q}, S_q = prod_{q<r<q0+C} * suf
+      md::mdv<K> P = pre;
+      for (int q = q0; q < min(m, q0 + C); ++q) {
+        md::mdv<K> S = suf;
+        for (int r = min(m, q0 + C) - 1; r > q; --r) S = md::mul<K>(md::load<K>(x + (long long)vars[r] * d, xs, 0), S);
+        md::mdv<K> part = md::mul<K>(P, S);
+        const long long e = (long long)i * n + vars[q];
+        md::store<K>(A0q, lsA, e, md::fma_acc<K>(md::load<K>(A0q, lsA, e), c, part));
+        P = md::mul<K>(P, md::load<K>(x + (long long)vars[q] * d, xs, 0));
+      }
+      __syncwarp();
+    }
+  }
+}
+}  // namespace ns

@@ -29,10 +29,21 @@ ns_status launch_evaldiff(ns_system* s, const double* x, cudaStream_t st) {
 }
 
 template <int K>
-ns_status launch_qr(ns_system* s, cudaStream_t st) {
+ns_status launch_a0(ns_system* s, const double* x, cudaStream_t st) {
+  DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
+            s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
+  const int blocks = std::max(1, std::min(s->sms, (s->n + 3) / 4));
+  ns::a0_kernel<K><<<blocks, 128, 0, st>>>(ds, x, s->A0q);
+  s->last_launches += 1;
+  CK(cudaGetLastError());
+  return NS_OK;
+}
+
+template <int K>
+ns_status launch_qr(ns_system* s, const double* A0src, cudaStream_t st) {
   CK(cudaMemsetAsync(s->bar, 0, 2 * sizeof(unsigned), st));
   int n = s->n;
-  const double* A0 = s->A0;
+  const double* A0 = A0src;
   double *W = s->W, *vh = s->vhead, *be = s->beta, *rd = s->rdiag;
   unsigned *bar = s->bar, *stt = s->status;
   void* args[] = {&n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt};
@@ -198,7 +209,9 @@ ns_status Impl<K>::setup(ns_system* s) { return setup_grids<K>(s); }
 template <int K>
 ns_status Impl<K>::evaldiff(ns_system* s, const double* x, cudaStream_t st) { return launch_evaldiff<K>(s, x, st); }
 template <int K>
-ns_status Impl<K>::qr(ns_system* s, cudaStream_t st) { return launch_qr<K>(s, st); }
+ns_status Impl<K>::qr(ns_system* s, const double* A0src, cudaStream_t st) { return launch_qr<K>(s, A0src, st); }
+template <int K>
+ns_status Impl<K>::a0(ns_system* s, const double* x, cudaStream_t st) { return launch_a0<K>(s, x, st); }
 template <int K>
 ns_status Impl<K>::stage(ns_system* s, int k_lo, cudaStream_t st) { return launch_stage<K>(s, k_lo, st); }
 template <int K>

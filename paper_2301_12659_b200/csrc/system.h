@@ -41,8 +41,12 @@ struct ns_system {
   bool qr_cached = false;
   cudaStream_t last_stream = nullptr;
   // ledger
-  static constexpr int LRING = 64;           // pending ledger records (5 events each)
-  cudaEvent_t ev[LRING][5] = {};
+  static constexpr int LRING = 64;           // pending ledger records (6 events each)
+  cudaEvent_t ev[LRING][6] = {};
+  // side stream: eval/diff runs there while A_0 -> QR runs on the caller's stream
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  double* A0q = nullptr;  // dense A_0 as factored (a0_kernel or ns_toeplitz_solve input)
   int ledger_head = 0, ledger_count = 0;     // ring of steps whose events are not yet read
   ns_ledger ledger{};
   int last_launches = 0;
@@ -58,7 +62,8 @@ template <int K>
 struct Impl {
   static ns_status setup(ns_system* s);
   static ns_status evaldiff(ns_system* s, const double* x, cudaStream_t st);
-  static ns_status qr(ns_system* s, cudaStream_t st);
+  static ns_status qr(ns_system* s, const double* A0src, cudaStream_t st);
+  static ns_status a0(ns_system* s, const double* x, cudaStream_t st);
   static ns_status stage(ns_system* s, int k_lo, cudaStream_t st);
   static ns_status residual(ns_system* s, double* x, double* res_out, cudaStream_t st);
   static ns_status batched(ns_system* s, int batch, double* x, const double* rhs, double* res,
