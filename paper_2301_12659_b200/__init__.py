@@ -32,7 +32,7 @@ EXPORTS = ["ns_system_create", "ns_system_destroy", "ns_newton_series_step",
            "ns_newton_series_step_batched", "ns_eval_diff", "ns_nnz", "ns_jacobian_pattern",
            "ns_toeplitz_solve", "ns_get_r_diag", "ns_md_op", "ns_get_status", "ns_get_ledger",
            "ns_reset_ledger", "ns_last_launch_count", "ns_strerror", "ns_build_info",
-           "ns_fp64_peak_probe"]
+           "ns_fp64_peak_probe", "ns_md_latency_probe"]
 
 
 class NSError(RuntimeError):
@@ -94,6 +94,7 @@ def lib() -> ctypes.CDLL:
         "ns_build_info": ([], ctypes.c_char_p),
         "ns_fp64_peak_probe": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                 ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+        "ns_md_latency_probe": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -266,3 +267,11 @@ def fp64_peak_probe(device: int = 0, op: str = "dfma") -> dict:
     _check(lib().ns_fp64_peak_probe(device, 0 if op == "dfma" else 1, ctypes.byref(g), ctypes.byref(ms)),
            "ns_fp64_peak_probe")
     return {"ginstr_per_s": g.value, "ms": ms.value}
+
+
+def md_latency_probe(precision: int, op: str = "fma") -> float:
+    """SM cycles per md operation in a dependent chain (one warp)."""
+    v = ctypes.c_double()
+    code = {"fma": 0, "add": 1, "mul": 2, "recip": 3, "sqrt": 4}[op]
+    _check(lib().ns_md_latency_probe(precision, code, ctypes.byref(v)), "ns_md_latency_probe")
+    return v.value

@@ -111,7 +111,7 @@ void free_all(ns_system* s) {
   void* ptrs[] = {s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst, s->row_ptr, s->col_idx, s->job_order,
                   s->coeff, s->rhs, s->b, s->A, s->A0, s->W, s->vhead, s->beta, s->rdiag, s->R, s->Qt,
                   s->invR, s->bp, s->dx, s->y, s->part, s->Minv, s->Z, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
-                  s->bar, s->status, s->bws, s->A0q, s->jobs, s->ser_off, s->pool, s->prog, s->left,
+                  s->bar, s->status, s->bws, s->A0q, s->qr_flags, s->jobs, s->ser_off, s->pool, s->prog, s->left,
                   s->left_init};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -266,6 +266,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->A, (size_t)K * d * s->nnz) == cudaSuccess;
   ok &= dalloc(&s->A0, (size_t)K * nn) == cudaSuccess;
   ok &= dalloc(&s->A0q, (size_t)K * nn) == cudaSuccess;
+  ok &= dalloc(&s->qr_flags, (size_t)n) == cudaSuccess;
   ok &= dalloc(&s->W, (size_t)K * 2 * nn) == cudaSuccess;
   ok &= dalloc(&s->vhead, (size_t)K * n) == cudaSuccess;
   ok &= dalloc(&s->beta, (size_t)K * n) == cudaSuccess;
@@ -529,4 +530,14 @@ extern "C" ns_status ns_fp64_peak_probe(int device, int op, double* ginstr, doub
   *ginstr = instr / (ms * 1e-3) * 1e-9;
   if (ms_out) *ms_out = ms / 5.0;
   return NS_OK;
+}
+
+extern "C" ns_status ns_md_latency_probe(int precision, int op, double* cycles_per_op) {
+  if (!cycles_per_op || op < 0 || op > 4) return NS_EINVAL;
+  switch (precision) {
+    case 2: return Impl<2>::latency(op, 256, cycles_per_op);
+    case 4: return Impl<4>::latency(op, 256, cycles_per_op);
+    case 8: return Impl<8>::latency(op, 256, cycles_per_op);
+    default: return NS_EPREC;
+  }
 }

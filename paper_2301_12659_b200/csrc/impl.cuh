@@ -42,11 +42,13 @@ ns_status launch_a0(ns_system* s, const double* x, cudaStream_t st) {
 template <int K>
 ns_status launch_qr(ns_system* s, const double* A0src, cudaStream_t st) {
   CK(cudaMemsetAsync(s->bar, 0, 2 * sizeof(unsigned), st));
+  CK(cudaMemsetAsync(s->qr_flags, 0, sizeof(int) * s->n, st));
   int n = s->n;
   const double* A0 = A0src;
   double *W = s->W, *vh = s->vhead, *be = s->beta, *rd = s->rdiag;
   unsigned *bar = s->bar, *stt = s->status;
-  void* args[] = {&n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt};
+  int* fl = s->qr_flags;
+  void* args[] = {&n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl};
   CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_kernel<K>, dim3(s->grid_qr), dim3(128),
                                  args, 0, st));
   const long long tot = (long long)K * n * n;
@@ -203,6 +205,50 @@ __global__ void md_op_kernel(int op, int n, const double* a, const double* b, do
   }
 }
 }  // namespace
+
+namespace {
+// single-warp dependent chains of md ops, timed with the SM clock (latency probe)
+template <int K>
+__global__ void md_latency_kernel(int op, int iters, const double* in, double* out, long long* cycles) {
+  md::mdv<K> a = md::load<K>(in, 4, 0), b = md::load<K>(in, 4, 1), c = md::load<K>(in, 4, 2);
+  __syncwarp();
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    switch (op) {
+      case 0: c = md::fma_acc<K>(c, a, b); break;
+      case 1: c = md::add<K>(c, a); break;
+      case 2: c = md::mul<K>(c, a); break;
+      case 3: c = md::recip<K>(c); break;
+      default: c = md::sqrt<K>(md::absv<K>(c)); break;
+    }
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) {
+    md::store<K>(out, 1, 0, c);
+    cycles[0] = t1 - t0;
+  }
+}
+}  // namespace
+
+template <int K>
+ns_status Impl<K>::latency(int op, int iters, double* cycles_per_op) {
+  double* buf = nullptr;
+  long long* cyc = nullptr;
+  CK(cudaMalloc(&buf, sizeof(double) * (4 * K + K)));
+  CK(cudaMalloc(&cyc, sizeof(long long)));
+  double h[4 * K];
+  for (int l = 0; l < K; ++l)
+    for (int e = 0; e < 4; ++e) h[l * 4 + e] = (l == 0) ? (e == 0 ? 0.999 : (e == 1 ? 1.0001 : 0.5)) : 0.0;
+  CK(cudaMemcpy(buf, h, sizeof(h), cudaMemcpyHostToDevice));
+  md_latency_kernel<K><<<1, 32>>>(op, 8, buf, buf + 4 * K, cyc);  // warm-up
+  md_latency_kernel<K><<<1, 32>>>(op, iters, buf, buf + 4 * K, cyc);
+  long long c = 0;
+  CK(cudaMemcpy(&c, cyc, sizeof(c), cudaMemcpyDeviceToHost));
+  cudaFree(buf);
+  cudaFree(cyc);
+  *cycles_per_op = (double)c / iters;
+  return NS_OK;
+}
 
 template <int K>
 ns_status Impl<K>::setup(ns_system* s) { return setup_grids<K>(s); }

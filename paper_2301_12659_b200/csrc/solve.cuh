@@ -89,16 +89,58 @@ __device__ void apply_reflector(int n, int j, int c, double* W, const double* vh
   }
 }
 
-// One Householder step per grid barrier; the owner of column j+1 applies H_j to
-// it first and then forms reflector j+1 (look-ahead of one column).
+// Reflector jj from sigma = sum_{r >= jj} x_r^2 (already reduced over the
+// warp) and x0 = x_jj: alpha = -sign(x0) sqrt(sigma), v0 = x0 - alpha,
+// beta = -1/(alpha v0); writes vhead, beta, rdiag and W[jj][jj] = alpha.
+template <int K>
+__device__ void reflector_from_sigma(int n, int jj, const md::mdv<K>& sig, const md::mdv<K>& x0, double* W,
+                                     double* vhead, double* beta, double* rdiag, unsigned* status) {
+  const long long ls = 2LL * n * n;
+  const int lane = lane_id();
+  const md::mdv<K> nrm = md::sqrt<K>(sig);
+  const md::mdv<K> alpha = md::is_negative<K>(x0) ? nrm : md::neg<K>(nrm);
+  const md::mdv<K> v0 = md::sub<K>(x0, alpha);
+  md::mdv<K> bt = md::zero<K>();
+  if (!md::is_zero<K>(sig)) bt = md::neg<K>(md::recip<K>(md::mul<K>(alpha, v0)));
+  else if (lane == 0 && status) atomicOr(status, ST_SINGULAR);
+  if (lane == 0) {
+    md::store_cg<K>(vhead, n, jj, v0);
+    md::store_cg<K>(beta, n, jj, bt);
+    md::store_cg<K>(rdiag, n, jj, alpha);
+    md::store_cg<K>(W, ls, (long long)jj * n + jj, alpha);
+  }
+}
+
+__device__ __forceinline__ void flag_wait(const int* f, int v) {
+  int ns = 16;
+  for (;;) {
+    int cur;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(cur) : "l"(f) : "memory");
+    if (cur >= v) break;
+    __nanosleep(ns);
+    ns = min(ns * 2, 256);
+  }
+}
+__device__ __forceinline__ void flag_set(int* f, int v) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
+
+// Householder QR of [A0 | I] (column major, ncol = 2n), one warp per column
+// (columns dealt round robin over the co-resident warps).  No grid barrier per
+// column: reflector j is published with a release flag; a warp applies H_j to
+// its columns once it acquires flag j.  The owner of column j+1 updates that
+// column first, keeps it in registers and builds reflector j+1 at once
+// (look-ahead of one column), so the critical path is one column update plus
+// one reflector per step.  n <= 128 rows per lane-register window (4 x 32).
 template <int K>
 __global__ void __launch_bounds__(128) householder_qr_kernel(int n, const double* __restrict__ A0,
                                                              double* W, double* vhead, double* beta,
                                                              double* rdiag, unsigned* bar,
-                                                             unsigned* status) {
+                                                             unsigned* status, int* flags) {
   const int ncol = 2 * n;
   const long long ls = (long long)ncol * n;
-  const int gw = gwarp(), nw = nwarps();
+  const int gw = gwarp(), nw = nwarps(), lane = lane_id();
   // W = [A0 | I], column major
   const long long tot = (long long)K * ncol * n;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
@@ -112,19 +154,53 @@ __global__ void __launch_bounds__(128) householder_qr_kernel(int n, const double
     __stcg(W + (long long)l * ls + (long long)c * n + r, v);
   }
   grid_sync(bar);
-  if (gw == 0) make_reflector<K>(n, 0, W, vhead, beta, rdiag, status);
-  grid_sync(bar);
+  if (gw == 0) {  // reflector 0 (owner of column 0)
+    md::mdv<K> sig = md::zero<K>();
+    for (int r = lane; r < n; r += 32) {
+      const md::mdv<K> v = md::load_cg<K>(W, ls, r);
+      sig = md::fma_acc<K>(sig, v, v);
+    }
+    sig = md::group_sum<K>(sig, 32);
+    reflector_from_sigma<K>(n, 0, sig, md::load_cg<K>(W, ls, 0), W, vhead, beta, rdiag, status);
+    __syncwarp();
+    if (lane == 0) flag_set(flags + 0, 1);
+  }
   for (int j = 0; j < n; ++j) {
-    const int look = j + 1;
-    if (look < n && (look % nw) == gw) {
-      apply_reflector<K>(n, j, look, W, vhead, beta);
-      __syncwarp();
-      make_reflector<K>(n, look, W, vhead, beta, rdiag, status);
+    // first owned column > j
+    int c = gw;
+    if (c <= j) c += ((j - gw) / nw + 1) * nw;
+    if (c >= ncol) break;  // nothing left for this warp
+    flag_wait(flags + j, 1);
+    __syncwarp();
+    const md::mdv<K> v0 = md::load_cg<K>(vhead, n, j);
+    const md::mdv<K> bt = md::load_cg<K>(beta, n, j);
+    for (; c < ncol; c += nw) {
+      // column c -= beta_j v (v^T column c), rows j..n-1
+      md::mdv<K> dot = md::zero<K>();
+      for (int r = j + lane; r < n; r += 32) {
+        const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
+        dot = md::fma_acc<K>(dot, v, md::load_cg<K>(W, ls, (long long)c * n + r));
+      }
+      dot = md::group_sum<K>(dot, 32);
+      const md::mdv<K> nw_ = md::neg<K>(md::mul<K>(bt, dot));
+      const bool look = (c == j + 1 && c < n);
+      md::mdv<K> sig = md::zero<K>(), x0 = md::zero<K>();
+      for (int r = j + lane; r < n; r += 32) {
+        const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
+        const md::mdv<K> w = md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)c * n + r), nw_, v);
+        md::store_cg<K>(W, ls, (long long)c * n + r, w);
+        if (look && r > j) sig = md::fma_acc<K>(sig, w, w);  // look-ahead norm, same pass
+        if (r == j + 1) x0 = w;
+      }
+      if (look) {
+        // rows j+1..n-1 of the updated column are the next reflector's x
+        sig = md::group_sum<K>(sig, 32);
+        x0 = md::shfl<K>(x0, (j + 1 - j) & 31);  // row j+1 lives in lane 1
+        reflector_from_sigma<K>(n, j + 1, sig, x0, W, vhead, beta, rdiag, status);
+        __syncwarp();
+        if (lane == 0) flag_set(flags + j + 1, 1);
+      }
     }
-    for (int c = gw; c < ncol; c += nw) {
-      if (c > j && (c != look || look >= n)) apply_reflector<K>(n, j, c, W, vhead, beta);
-    }
-    grid_sync(bar);
   }
 }
 

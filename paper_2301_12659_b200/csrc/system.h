@@ -46,7 +46,8 @@ struct ns_system {
   // side stream: eval/diff runs there while A_0 -> QR runs on the caller's stream
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  double* A0q = nullptr;  // dense A_0 as factored (a0_kernel or ns_toeplitz_solve input)
+  double* A0q = nullptr;
+  int* qr_flags = nullptr;  // [n] reflector-ready flags of the QR kernel  // dense A_0 as factored (a0_kernel or ns_toeplitz_solve input)
   int ledger_head = 0, ledger_count = 0;     // ring of steps whose events are not yet read
   ns_ledger ledger{};
   int last_launches = 0;
@@ -69,6 +70,7 @@ struct Impl {
   static ns_status batched(ns_system* s, int batch, double* x, const double* rhs, double* res,
                            uint32_t flags, cudaStream_t st);
   static ns_status md_op(int op, int n, const double* a, const double* b, double* c, cudaStream_t st);
+  static ns_status latency(int op, int iters, double* cycles_per_op);
 };
 
 #define NS_CK(x)                               \
