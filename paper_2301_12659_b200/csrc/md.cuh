@@ -134,17 +134,16 @@ MD_INL void level_insert(double (&s)[K], int l, double t) {
   s[K - 1] = dadd(s[K - 1], t);
 }
 
-// Fused accumulate r = acc + a*b.  The products a_i b_j with i + j = l and the
+// Level sums of the product a*b: the products a_i b_j with i + j = l and the
 // two_prod errors of the products of level l - 1 enter level l; level K-1
-// products are formed with FMA into the last level.  Cost for K = 4: 14 two_sum
-// + 6 two_prod + 4 FMA + renorm; K = 8: 140 two_sum + 28 two_prod + 8 FMA + renorm.
+// products are formed with FMA into the last level.  s is NOT normalised.
 template <int K>
-MD_INL mdv<K> fma_acc(const mdv<K>& acc, const mdv<K>& a, const mdv<K>& b) {
-  double s[K];
+MD_INL void prod_levels(const mdv<K>& a, const mdv<K>& b, double (&s)[K]) {
+  two_prod(a.x[0], b.x[0], s[0], s[1]);
 #pragma unroll
-  for (int l = 0; l < K; ++l) s[l] = acc.x[l];
+  for (int l = 2; l < K; ++l) s[l] = 0.0;
 #pragma unroll
-  for (int l = 0; l < K - 1; ++l) {
+  for (int l = 1; l < K - 1; ++l) {
 #pragma unroll
     for (int i = 0; i <= l; ++i) {
       double p, e;
@@ -155,6 +154,20 @@ MD_INL mdv<K> fma_acc(const mdv<K>& acc, const mdv<K>& a, const mdv<K>& b) {
   }
 #pragma unroll
   for (int i = 0; i < K; ++i) s[K - 1] = dfma(a.x[i], b.x[K - 1 - i], s[K - 1]);
+}
+
+// Fused accumulate r = acc + a*b.  The product's level sums do not depend on
+// acc; acc joins last (K level inserts + renorm), so in a dependent chain
+// (a dot product) only the add is on the critical path and the next product
+// overlaps it.  Cost K = 4: 20 two_sum + 6 two_prod + 4 FMA + 4 DADD + renorm;
+// K = 8: 168 two_sum + 28 two_prod + 8 FMA + 8 DADD + renorm (csrc/md.cuh counts
+// in perfmodel.py).
+template <int K>
+MD_INL mdv<K> fma_acc(const mdv<K>& acc, const mdv<K>& a, const mdv<K>& b) {
+  double s[K];
+  prod_levels<K>(a, b, s);
+#pragma unroll
+  for (int l = 0; l < K; ++l) level_insert<K>(s, l, acc.x[l]);
   return renorm<K, K>(s);
 }
 
@@ -176,7 +189,9 @@ MD_INL mdv<K> sub(const mdv<K>& a, const mdv<K>& b) {
 
 template <int K>
 MD_INL mdv<K> mul(const mdv<K>& a, const mdv<K>& b) {
-  return fma_acc<K>(zero<K>(), a, b);
+  double s[K];
+  prod_levels<K>(a, b, s);
+  return renorm<K, K>(s);
 }
 
 // ---------------------------------------------------------------- double-double

@@ -11,14 +11,17 @@ Numerators (always labelled):
 """
 from __future__ import annotations
 
-# FP64 instructions of one md fused accumulate r = acc + a*b (csrc/md.cuh fma_acc)
+# FP64 instructions of one md fused accumulate r = acc + a*b (csrc/md.cuh fma_acc:
+# product level sums, then acc inserted, then renorm)
 #   K=2: two_prod (DMUL+DFMA) + 2 DFMA + two_sum (6) + 2 DADD + fast_two_sum (3)
-#   K=4: 20 two_sum + 12 DADD + 6 two_prod + 4 DFMA       (cascade 14 + renorm 6)
-#   K=8: 154 two_sum + 56 DADD + 28 two_prod + 8 DFMA     (cascade 140 + renorm 14)
+#   K=4: product 9 two_sum + 10 DADD, acc 6 two_sum + 4 DADD, renorm 6 two_sum;
+#        6 two_prod + 4 DFMA                               -> 140 DADD, 6 DMUL, 10 DFMA
+#   K=8: product 127 two_sum + 54 DADD, acc 28 two_sum + 8 DADD, renorm 14 two_sum;
+#        28 two_prod + 8 DFMA                              -> 1076 DADD, 28 DMUL, 36 DFMA
 MD_FMA_MIX = {
     2: dict(dadd=11, dmul=1, dfma=3),
-    4: dict(dadd=20 * 6 + 12, dmul=6, dfma=6 + 4),
-    8: dict(dadd=154 * 6 + 56, dmul=28, dfma=28 + 8),
+    4: dict(dadd=21 * 6 + 14, dmul=6, dfma=6 + 4),
+    8: dict(dadd=169 * 6 + 62, dmul=28, dfma=28 + 8),
 }
 # md add: K(K-1)/2 cascade two_sum + K DADD + renorm 2(K-1) two_sum (K=2 specialised: 11)
 MD_ADD_MIX = {2: dict(dadd=11, dmul=0, dfma=0),
