@@ -38,7 +38,8 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3"])
+    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C5"])
+    p.add_argument("--batch", type=int, default=4096, help="C5: total paths (partitioned over ranks)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
     return p.parse_args()
@@ -207,6 +208,115 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ C5: batch of paths
+def _c5_path(p):
+    import synth
+    sys_ = synth.triangular_system(32, 15, 2, seed=12665 + p, name="C5")
+    return synth.make_x(sys_, "near", seed=100 + p), sys_.rhs
+
+
+def run_c5(args):
+    """BASELINE configs[4]: 4096 independent paths (dim 32, degree 15, double
+    double), paths partitioned across ranks (dist.partition), one
+    ns_newton_series_step_batched per rank per step; no collective in the step.
+    Strong scaling: the total batch is fixed."""
+    import multiprocessing as mp
+
+    import numpy as np
+    import torch
+
+    import paper_2301_12659_b200 as P
+    import synth
+    from paper_2301_12659_b200 import perfmodel as PM
+    from paper_2301_12659_b200.dist import max_over_ranks, partition
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    lo, hi = partition(args.batch, ws, rank)
+    with mp.Pool(min(16, os.cpu_count() or 1)) as pool:
+        data = pool.map(_c5_path, range(lo, hi), chunksize=16)
+    base = synth.triangular_system(32, 15, 2, seed=12665, name="C5")
+    dev = torch.device(f"cuda:{local}")
+    X0 = torch.tensor(np.stack([d[0] for d in data]), device=dev)
+    R = torch.tensor(np.stack([d[1] for d in data]), device=dev)
+    X = X0.clone()
+    B = hi - lo
+    res = torch.zeros((B, 2, 3), dtype=torch.float64, device=dev)
+    h = P.NewtonSystem.from_system(base, max_batch=max(1, B), device=local)
+    c, per_class, total = work(base, h.nnz)
+    flops_path = PM.flops(total, 2)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        X.copy_(X0)
+        h.step_batched(X, R, res)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        X.copy_(X0)
+        flush.zero_()
+        ev[i][0].record(stream)
+        h.step_batched(X, R, res)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    ms_total = sum(a.elapsed_time(b) for a, b in ev)
+    # e2e: pinned host x and rhs in, x and residuals out, every step
+    Xh = X0.cpu().pin_memory(); Rh = R.cpu().pin_memory()
+    Xo = torch.empty_like(Xh).pin_memory(); Ro = torch.empty((B, 2, 3), dtype=torch.float64).pin_memory()
+    ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        ee[i][0].record(stream)
+        X.copy_(Xh, non_blocking=True)
+        R.copy_(Rh, non_blocking=True)
+        h.step_batched(X, R, res)
+        Xo.copy_(X, non_blocking=True)
+        Ro.copy_(res, non_blocking=True)
+        ee[i][1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in ee)
+    ms_total = max_over_ranks(ms_total, dev)
+    e2e_ms = max_over_ranks(e2e_ms, dev)
+    ms_step = ms_total / args.steps
+    value = args.batch * flops_path / (ms_step * 1e-3) * 1e-9
+    probe = P.fp64_peak_probe(local, "dfma")
+    peak = 2.0 * probe["ginstr_per_s"]
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded per path, synth.py; 'near' start series)",
+        "config": {"workload": f"C5: batch of {args.batch} independent paths, dim=32 one-column monomial "
+                               f"system, degree 15, double double, one Newton step per path",
+                   "batch": args.batch, "parallelism": f"paths partitioned x{ws}",
+                   "l2": "flushed (256 MiB memset) before every timed step"},
+        "paths_per_s": args.batch / (ms_step * 1e-3),
+        "pct_of_peak": 100.0 * value / (ws * peak),
+        "e2e": {"value": args.batch * flops_path / (e2e_ms / args.steps * 1e-3) * 1e-9, "unit": UNIT,
+                "h2d_bytes_per_step": (Xh.numel() + Rh.numel()) * 8 * ws,
+                "d2h_bytes_per_step": (Xo.numel() + Ro.numel()) * 8 * ws, "ms_per_step": e2e_ms / args.steps},
+        "roofline": {"bound": "alu", "kernel_class": "batched_step", "achieved": value / ws, "peak": peak,
+                     "unit": "GFLOP/s", "frac": value / ws / peak, "traffic": None,
+                     "peak_source": "measured DFMA-chain probe x2"},
+        "gpu_launches": args.steps,
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     import numpy as np
@@ -352,6 +462,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "C5":
+        run_c5(args)
     else:
         run_ours(args)
 

@@ -50,7 +50,7 @@ ns_status launch_qr(ns_system* s, const double* A0src, cudaStream_t st) {
   int* fl = s->qr_flags;
   void* args[] = {&n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl};
   CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_kernel<K>, dim3(s->grid_qr), dim3(128),
-                                 args, 0, st));
+                                 args, s->qr_smem_reserve, st));
   const long long tot = (long long)K * n * n;
   const int blocks = (int)std::min<long long>((tot + 255) / 256, 4LL * s->sms);
   ns::qr_unpack_kernel<K><<<blocks, 256, 0, st>>>(n, s->W, s->R, s->Qt);
@@ -107,6 +107,19 @@ ns_status setup_grids(ns_system* s) {
   // cooperative grids: enough warps for the 2n columns of [A0 | I], never more
   // CTAs than SMs (a grid barrier costs more with every CTA); env overrides for tuning
   s->grid_qr = std::min(s->sms, std::max(1, (2 * s->n + 3) / 4));
+  // The QR is latency-bound and runs concurrently with eval/diff; a large
+  // dynamic shared-memory request keeps eval/diff CTAs off the QR's SMs
+  // (NS_QR_RESERVE=0 disables).  Default: reserve when the QR grid is small
+  // relative to the GPU.
+  {
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->dev));
+    bool reserve = 4 * s->grid_qr <= s->sms;
+    if (const char* e = getenv("NS_QR_RESERVE")) reserve = atoi(e) != 0;
+    s->qr_smem_reserve = reserve ? (size_t)optin : 0;
+    if (reserve)
+      CK(cudaFuncSetAttribute(ns::householder_qr_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  }
   if (const char* e = getenv("NS_QR_GRID")) s->grid_qr = std::max(1, std::min(s->sms * occ, atoi(e)));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::stage_kernel<K>, 128, 0));
   if (occ < 1) return NS_ECUDA;

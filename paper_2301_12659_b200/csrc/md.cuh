@@ -171,6 +171,29 @@ MD_INL mdv<K> fma_acc(const mdv<K>& acc, const mdv<K>& a, const mdv<K>& b) {
   return renorm<K, K>(s);
 }
 
+// Same operation with acc entering first (it seeds the level sums): shorter
+// latency when the dependence runs through a or b (Newton iterations of
+// recip / rsqrt), longer through acc.
+template <int K>
+MD_INL mdv<K> fma_acc_first(const mdv<K>& acc, const mdv<K>& a, const mdv<K>& b) {
+  double s[K];
+#pragma unroll
+  for (int l = 0; l < K; ++l) s[l] = acc.x[l];
+#pragma unroll
+  for (int l = 0; l < K - 1; ++l) {
+#pragma unroll
+    for (int i = 0; i <= l; ++i) {
+      double p, e;
+      two_prod(a.x[i], b.x[l - i], p, e);
+      level_insert<K>(s, l, p);
+      level_insert<K>(s, l + 1, e);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) s[K - 1] = dfma(a.x[i], b.x[K - 1 - i], s[K - 1]);
+  return renorm<K, K>(s);
+}
+
 // r = a + b with the same level accumulator.
 template <int K>
 MD_INL mdv<K> add(const mdv<K>& a, const mdv<K>& b) {
@@ -241,34 +264,55 @@ MD_INL mdv<P> trunc(const mdv<K>& a) {
   return r;
 }
 
-// 1/b: y <- y + y (1 - b y)
+// 1/b: y = y_h + y_h (1 - b y_h), y_h = 1/b at K/2 limbs.  The residual
+// e = 1 - b y_h is formed in K limbs; the correction y_h e only needs K/2 limbs
+// (it is 2^(-53K/2) times smaller), so the critical path is
+// recip<K/2> + fma<K> + mul<K/2> + add<K>.
 template <int K>
 MD_INL mdv<K> recip(const mdv<K>& b) {
-  mdv<K> y;
   if constexpr (K == 2) {
-    y = from_double<2>(1.0 / b.x[0]);
+    const double y0 = 1.0 / b.x[0];
+    const mdv<2> e = fma_acc_first<2>(from_double<2>(1.0), neg<2>(b), from_double<2>(y0));
+    mdv<2> r;
+    fast_two_sum(y0, dmul(y0, e.x[0]), r.x[0], r.x[1]);
+    return r;
   } else {
-    y = trunc<K, K / 2>(recip<K / 2>(trunc<K / 2, K>(b)));
+    const mdv<K / 2> yh = recip<K / 2>(trunc<K / 2, K>(b));
+    const mdv<K> e = fma_acc_first<K>(from_double<K>(1.0), neg<K>(b), trunc<K, K / 2>(yh));
+    const mdv<K / 2> corr = mul<K / 2>(yh, trunc<K / 2, K>(e));
+    return add<K>(trunc<K, K / 2>(yh), trunc<K, K / 2>(corr));
   }
-  mdv<K> e = fma_acc<K>(from_double<K>(1.0), neg<K>(b), y);  // 1 - b y
-  return fma_acc<K>(y, y, e);
 }
 
-// 1/sqrt(a), a > 0: y <- y + (y/2) (1 - a y^2)
+// sqrt(a), a >= 0: s = s_h + (a - s_h^2) / (2 s_h), s_h = sqrt at K/2 limbs; the
+// residual in K limbs, the quotient in K/2 limbs (Karp-Markstein).  recip of
+// 2 s_h runs alongside the residual.
+template <int K>
+MD_INL mdv<K> sqrt(const mdv<K>& a) {
+  if (!(a.x[0] > 0.0)) return zero<K>();
+  if constexpr (K == 2) {
+    const double s0 = ::sqrt(a.x[0]);
+    const mdv<2> r = fma_acc_first<2>(a, from_double<2>(-s0), from_double<2>(s0));
+    mdv<2> out;
+    fast_two_sum(s0, r.x[0] / (2.0 * s0), out.x[0], out.x[1]);
+    return out;
+  } else {
+    const mdv<K / 2> sh = sqrt<K / 2>(trunc<K / 2, K>(a));
+    mdv<K / 2> two_sh = sh;
+#pragma unroll
+    for (int i = 0; i < K / 2; ++i) two_sh.x[i] = 2.0 * sh.x[i];
+    const mdv<K / 2> inv2 = recip<K / 2>(two_sh);
+    const mdv<K> shK = trunc<K, K / 2>(sh);
+    const mdv<K> r = fma_acc_first<K>(a, neg<K>(shK), shK);  // a - s_h^2
+    const mdv<K / 2> corr = mul<K / 2>(trunc<K / 2, K>(r), inv2);
+    return add<K>(shK, trunc<K, K / 2>(corr));
+  }
+}
+
+// 1/sqrt(a) = recip(sqrt(a)) (not on a hot path)
 template <int K>
 MD_INL mdv<K> rsqrt(const mdv<K>& a) {
-  mdv<K> y;
-  if constexpr (K == 2) {
-    y = from_double<2>(1.0 / ::sqrt(a.x[0]));
-  } else {
-    y = trunc<K, K / 2>(rsqrt<K / 2>(trunc<K / 2, K>(a)));
-  }
-  mdv<K> t = mul<K>(y, y);
-  mdv<K> e = fma_acc<K>(from_double<K>(1.0), neg<K>(a), t);  // 1 - a y^2
-  mdv<K> h;
-#pragma unroll
-  for (int i = 0; i < K; ++i) h.x[i] = 0.5 * y.x[i];
-  return fma_acc<K>(y, h, e);
+  return recip<K>(sqrt<K>(a));
 }
 
 // a / b = q + y (a - q b), q = a y, y = 1/b (Markstein correction)
@@ -276,21 +320,8 @@ template <int K>
 MD_INL mdv<K> div(const mdv<K>& a, const mdv<K>& b) {
   const mdv<K> y = recip<K>(b);
   const mdv<K> q = mul<K>(a, y);
-  const mdv<K> r = fma_acc<K>(a, neg<K>(q), b);
-  return fma_acc<K>(q, y, r);
-}
-
-// sqrt(a), a >= 0: s = a y, s + (y/2)(a - s^2), y = 1/sqrt(a) (Karp-Markstein)
-template <int K>
-MD_INL mdv<K> sqrt(const mdv<K>& a) {
-  if (!(a.x[0] > 0.0)) return zero<K>();
-  const mdv<K> y = rsqrt<K>(a);
-  const mdv<K> s0 = mul<K>(a, y);
-  const mdv<K> r = fma_acc<K>(a, neg<K>(s0), s0);
-  mdv<K> h;
-#pragma unroll
-  for (int i = 0; i < K; ++i) h.x[i] = 0.5 * y.x[i];
-  return fma_acc<K>(s0, h, r);
+  const mdv<K> r = fma_acc_first<K>(a, neg<K>(q), b);
+  return fma_acc_first<K>(q, y, r);
 }
 
 // sign of an md value (leading nonzero limb decides; limbs are nonoverlapping)
