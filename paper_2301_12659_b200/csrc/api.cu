@@ -47,22 +47,20 @@ ns_status step_impl(ns_system* s, double* x, double* res_out, uint32_t flags, cu
     ev = s->ev[(s->ledger_head + s->ledger_count) % ns_system::LRING];
     CK(cudaEventRecord(ev[0], st));
   }
+  // the QR (which forms A_0 itself) is launched first so that its co-resident
+  // grid is placed before eval/diff fills the SMs
   CK(cudaEventRecord(s->ev_fork, st));
   CK(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
   ns_status r;
   if (!(flags & NS_REUSE_QR)) {
-    r = Impl<K>::a0(s, x, st);
+    r = Impl<K>::qr(s, nullptr, x, st);
     if (r) return r;
   }
+  if (ledger) CK(cudaEventRecord(ev[2], st));
   r = Impl<K>::evaldiff(s, x, s->side);
   if (r) return r;
   if (ledger) CK(cudaEventRecord(ev[1], s->side));
   CK(cudaEventRecord(s->ev_join, s->side));
-  if (!(flags & NS_REUSE_QR)) {
-    r = Impl<K>::qr(s, s->A0q, st);
-    if (r) return r;
-  }
-  if (ledger) CK(cudaEventRecord(ev[2], st));
   CK(cudaStreamWaitEvent(st, s->ev_join, 0));
   if (ledger) CK(cudaEventRecord(ev[3], st));
   r = Impl<K>::stage(s, 0, st);
@@ -267,6 +265,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->A0, (size_t)K * nn) == cudaSuccess;
   ok &= dalloc(&s->A0q, (size_t)K * nn) == cudaSuccess;
   ok &= dalloc(&s->qr_flags, (size_t)n) == cudaSuccess;
+  ok &= cudaMemset(s->qr_flags, 0, sizeof(int) * n) == cudaSuccess;
   ok &= dalloc(&s->W, (size_t)K * 2 * nn) == cudaSuccess;
   ok &= dalloc(&s->vhead, (size_t)K * n) == cudaSuccess;
   ok &= dalloc(&s->beta, (size_t)K * n) == cudaSuccess;
@@ -418,9 +417,9 @@ ns_status ns_toeplitz_solve(ns_system* s, const double* b, const double* A, cons
   s->last_launches = 0;
   s->use_m = true;
   switch (s->K) {
-    case 2: r = Impl<2>::qr(s, s->A0q, st); if (!r) r = Impl<2>::stage(s, 0, st); break;
-    case 4: r = Impl<4>::qr(s, s->A0q, st); if (!r) r = Impl<4>::stage(s, 0, st); break;
-    default: r = Impl<8>::qr(s, s->A0q, st); if (!r) r = Impl<8>::stage(s, 0, st); break;
+    case 2: r = Impl<2>::qr(s, s->A0q, nullptr, st); if (!r) r = Impl<2>::stage(s, 0, st); break;
+    case 4: r = Impl<4>::qr(s, s->A0q, nullptr, st); if (!r) r = Impl<4>::stage(s, 0, st); break;
+    default: r = Impl<8>::qr(s, s->A0q, nullptr, st); if (!r) r = Impl<8>::stage(s, 0, st); break;
   }
   if (r) return r;
   CK(cudaMemcpyAsync(dx, s->dx, sizeof(double) * K * d * n, cudaMemcpyDeviceToDevice, st));

@@ -276,45 +276,47 @@ __device__ md::mdv<K> warp_excl_scan_mul(md::mdv<K> v) {
   return lane == 0 ? md::from_double<K>(1.0) : e;
 }
 
+// Row i of A_0 into dst[(l * plane) + i * rs + j * cs] (row-major: rs = n, cs = 1;
+// column-major W: rs = 1, cs = n), one warp.
+template <int K>
+__device__ void a0_row(const DevSys& s, const double* __restrict__ x, int i, double* dst, long long plane,
+                       long long rs, long long cs) {
+  const int n = s.n, d = s.d;
+  const long long xs = (long long)n * d;
+  const int lane = threadIdx.x & 31;
+  for (int j = lane; j < n; j += 32) md::store<K>(dst, plane, i * rs + j * cs, md::zero<K>());
+  __syncwarp();
+  for (int tau = s.eq_ptr[i]; tau < s.eq_ptr[i + 1]; ++tau) {
+    const int m0 = s.mono_ptr[tau], m = s.mono_ptr[tau + 1] - m0;
+    const int* vars = s.var_idx + m0;
+    md::mdv<K> c;
+#pragma unroll
+    for (int l = 0; l < K; ++l) c.x[l] = s.coeff[(long long)l * s.M + tau];
+    const int C = (m + 31) / 32;  // chunk per lane
+    const int q0 = lane * C;
+    md::mdv<K> lp = md::from_double<K>(1.0), ls = md::from_double<K>(1.0);
+    for (int q = q0; q < min(m, q0 + C); ++q) lp = md::mul<K>(lp, md::load<K>(x + (long long)vars[q] * d, xs, 0));
+    for (int q = min(m, q0 + C) - 1; q >= q0; --q) ls = md::mul<K>(md::load<K>(x + (long long)vars[q] * d, xs, 0), ls);
+    const md::mdv<K> pre = warp_excl_scan_mul<K>(lp);
+    const md::mdv<K> rv = md::shfl<K>(ls, 31 - lane);
+    const md::mdv<K> sufr = warp_excl_scan_mul<K>(rv);
+    const md::mdv<K> suf = md::shfl<K>(sufr, 31 - lane);
+    md::mdv<K> P = pre;
+    for (int q = q0; q < min(m, q0 + C); ++q) {
+      md::mdv<K> S = suf;
+      for (int r = min(m, q0 + C) - 1; r > q; --r) S = md::mul<K>(md::load<K>(x + (long long)vars[r] * d, xs, 0), S);
+      const md::mdv<K> part = md::mul<K>(P, S);
+      const long long e = i * rs + (long long)vars[q] * cs;
+      md::store<K>(dst, plane, e, md::fma_acc<K>(md::load<K>(dst, plane, e), c, part));
+      P = md::mul<K>(P, md::load<K>(x + (long long)vars[q] * d, xs, 0));
+    }
+    __syncwarp();
+  }
+}
+
 template <int K>
 __global__ void __launch_bounds__(128) a0_kernel(DevSys s, const double* __restrict__ x, double* __restrict__ A0q) {
-  const int n = s.n, d = s.d;
-  const long long xs = (long long)n * d, lsA = (long long)n * n;
-  const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (int i = gw; i < n; i += nw) {
-    for (int j = lane; j < n; j += 32) md::store<K>(A0q, lsA, (long long)i * n + j, md::zero<K>());
-    __syncwarp();
-    for (int tau = s.eq_ptr[i]; tau < s.eq_ptr[i + 1]; ++tau) {
-      const int m0 = s.mono_ptr[tau], m = s.mono_ptr[tau + 1] - m0;
-      const int* vars = s.var_idx + m0;
-      md::mdv<K> c;
-#pragma unroll
-      for (int l = 0; l < K; ++l) c.x[l] = s.coeff[(long long)l * s.M + tau];
-      const int C = (m + 31) / 32;  // chunk per lane
-      const int q0 = lane * C;
-      // local exclusive prefix and suffix products inside the chunk
-      md::mdv<K> lp = md::from_double<K>(1.0), ls = md::from_double<K>(1.0);
-      for (int q = q0; q < min(m, q0 + C); ++q) lp = md::mul<K>(lp, md::load<K>(x + (long long)vars[q] * d, xs, 0));
-      for (int q = min(m, q0 + C) - 1; q >= q0; --q) ls = md::mul<K>(md::load<K>(x + (long long)vars[q] * d, xs, 0), ls);
-      // lanes' chunk products: prefix over lower lanes, suffix over higher lanes
-      md::mdv<K> pre = warp_excl_scan_mul<K>(lp);
-      // suffix scan: reverse the lane order
-      md::mdv<K> rv = md::shfl<K>(ls, 31 - lane);
-      md::mdv<K> sufr = warp_excl_scan_mul<K>(rv);
-      md::mdv<K> suf = md::shfl<K>(sufr, 31 - lane);
-      // walk the chunk: P_q = pre * prod_{q0<=r<q}, S_q = prod_{q<r<q0+C} * suf
-      md::mdv<K> P = pre;
-      for (int q = q0; q < min(m, q0 + C); ++q) {
-        md::mdv<K> S = suf;
-        for (int r = min(m, q0 + C) - 1; r > q; --r) S = md::mul<K>(md::load<K>(x + (long long)vars[r] * d, xs, 0), S);
-        md::mdv<K> part = md::mul<K>(P, S);
-        const long long e = (long long)i * n + vars[q];
-        md::store<K>(A0q, lsA, e, md::fma_acc<K>(md::load<K>(A0q, lsA, e), c, part));
-        P = md::mul<K>(P, md::load<K>(x + (long long)vars[q] * d, xs, 0));
-      }
-      __syncwarp();
-    }
-  }
+  for (int i = gw; i < s.n; i += nw) a0_row<K>(s, x, i, A0q, (long long)s.n * s.n, s.n, 1);
 }
 }  // namespace ns

@@ -39,16 +39,22 @@ ns_status launch_a0(ns_system* s, const double* x, cudaStream_t st) {
   return NS_OK;
 }
 
+// QR of A_0: from A0src (dense row-major) or, with x != nullptr, A_0 formed
+// from x inside the QR kernel.
 template <int K>
-ns_status launch_qr(ns_system* s, const double* A0src, cudaStream_t st) {
-  CK(cudaMemsetAsync(s->bar, 0, 2 * sizeof(unsigned), st));
-  CK(cudaMemsetAsync(s->qr_flags, 0, sizeof(int) * s->n, st));
+ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStream_t st) {
+  // no memsets before the launch: the grid barrier is self-resetting and the
+  // reflector flags carry an epoch (launch counter)
+  int epoch = ++s->qr_epoch;
   int n = s->n;
   const double* A0 = A0src;
   double *W = s->W, *vh = s->vhead, *be = s->beta, *rd = s->rdiag;
   unsigned *bar = s->bar, *stt = s->status;
   int* fl = s->qr_flags;
-  void* args[] = {&n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl};
+  DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
+            s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
+  const double* xp = x;
+  void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch};
   CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_kernel<K>, dim3(s->grid_qr), dim3(128),
                                  args, s->qr_smem_reserve, st));
   const long long tot = (long long)K * n * n;
@@ -268,7 +274,9 @@ ns_status Impl<K>::setup(ns_system* s) { return setup_grids<K>(s); }
 template <int K>
 ns_status Impl<K>::evaldiff(ns_system* s, const double* x, cudaStream_t st) { return launch_evaldiff<K>(s, x, st); }
 template <int K>
-ns_status Impl<K>::qr(ns_system* s, const double* A0src, cudaStream_t st) { return launch_qr<K>(s, A0src, st); }
+ns_status Impl<K>::qr(ns_system* s, const double* A0src, const double* x, cudaStream_t st) {
+  return launch_qr<K>(s, A0src, x, st);
+}
 template <int K>
 ns_status Impl<K>::a0(ns_system* s, const double* x, cudaStream_t st) { return launch_a0<K>(s, x, st); }
 template <int K>

@@ -360,25 +360,55 @@ MD_INL mdv<K> shfl(const mdv<K>& a, int src, int width = 32) {
 }
 // Butterfly sum over aligned groups of G lanes (G power of two <= 32).  Every
 // lane of the group ends with the same bits (the tree is symmetric: lane and
-// partner add in the same operand order, lower lane first).
+// partner add in the same operand order, lower lane first).  For K >= 4 the
+// intermediate sums stay as unnormalised level arrays (exact two_sum cascades,
+// plain adds only in the last level) and are renormalised once at the end.
 template <int K>
 MD_INL mdv<K> group_sum(mdv<K> v, int G) {
   const int lane = threadIdx.x & 31;
+  if constexpr (K == 2) {
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    if (off < G) {
-      mdv<K> o = shfl_xor<K>(v, off);
-      const bool hi = (lane & off) != 0;
-      mdv<K> lo_v, hi_v;
+    for (int off = 1; off < 32; off <<= 1) {
+      if (off < G) {
+        mdv<K> o = shfl_xor<K>(v, off);
+        const bool hi = (lane & off) != 0;
+        mdv<K> lo_v, hi_v;
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        lo_v.x[i] = hi ? o.x[i] : v.x[i];
-        hi_v.x[i] = hi ? v.x[i] : o.x[i];
+        for (int i = 0; i < K; ++i) {
+          lo_v.x[i] = hi ? o.x[i] : v.x[i];
+          hi_v.x[i] = hi ? v.x[i] : o.x[i];
+        }
+        v = add<K>(lo_v, hi_v);
       }
-      v = add<K>(lo_v, hi_v);
     }
+    return v;
+  } else {
+    double s[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) s[i] = v.x[i];
+    bool any = false;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      if (off < G) {
+        any = true;
+        double o[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) o[i] = __shfl_xor_sync(0xffffffffu, s[i], off);
+        const bool hi = (lane & off) != 0;
+        double lo_s[K], hi_s[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          lo_s[i] = hi ? o[i] : s[i];
+          hi_s[i] = hi ? s[i] : o[i];
+        }
+#pragma unroll
+        for (int i = 0; i < K; ++i) s[i] = lo_s[i];
+#pragma unroll
+        for (int l = 0; l < K; ++l) level_insert<K>(s, l, hi_s[l]);
+      }
+    }
+    return any ? renorm<K, K>(s) : v;
   }
-  return v;
 }
 
 // ---------------------------------------------------------------- memory (limb planes)

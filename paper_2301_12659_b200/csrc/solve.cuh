@@ -14,6 +14,7 @@
 // every md reduction has a fixed order (deterministic).
 #pragma once
 #include "common.cuh"
+#include "evaldiff.cuh"
 
 namespace ns {
 
@@ -134,25 +135,30 @@ __device__ __forceinline__ void flag_set(int* f, int v) {
 // (look-ahead of one column), so the critical path is one column update plus
 // one reflector per step.  n <= 128 rows per lane-register window (4 x 32).
 template <int K>
-__global__ void __launch_bounds__(128) householder_qr_kernel(int n, const double* __restrict__ A0,
+__global__ void __launch_bounds__(128) householder_qr_kernel(DevSys sy, const double* __restrict__ x, int n,
+                                                             const double* __restrict__ A0,
                                                              double* W, double* vhead, double* beta,
                                                              double* rdiag, unsigned* bar,
-                                                             unsigned* status, int* flags) {
+                                                             unsigned* status, int* flags, int epoch) {
   const int ncol = 2 * n;
   const long long ls = (long long)ncol * n;
   const int gw = gwarp(), nw = nwarps(), lane = lane_id();
-  // W = [A0 | I], column major
+  // W = [A0 | I], column major.  With x given, A_0 is formed here (warp per
+  // equation, a0_row) so the QR needs no eval/diff output and can start first.
   const long long tot = (long long)K * ncol * n;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
        t += (long long)gridDim.x * blockDim.x) {
     const int r = (int)(t % n);
     const long long lc = t / n;
     const int c = (int)(lc % ncol), l = (int)(lc / ncol);
+    if (c < n && x) continue;
     double v;
     if (c < n) v = A0[((long long)l * n + r) * n + c];
     else v = (l == 0 && r == c - n) ? 1.0 : 0.0;
     __stcg(W + (long long)l * ls + (long long)c * n + r, v);
   }
+  if (x)
+    for (int i = gw; i < n; i += nw) a0_row<K>(sy, x, i, W, ls, 1, n);
   grid_sync(bar);
   if (gw == 0) {  // reflector 0 (owner of column 0)
     md::mdv<K> sig = md::zero<K>();
@@ -163,14 +169,14 @@ __global__ void __launch_bounds__(128) householder_qr_kernel(int n, const double
     sig = md::group_sum<K>(sig, 32);
     reflector_from_sigma<K>(n, 0, sig, md::load_cg<K>(W, ls, 0), W, vhead, beta, rdiag, status);
     __syncwarp();
-    if (lane == 0) flag_set(flags + 0, 1);
+    if (lane == 0) flag_set(flags + 0, epoch);
   }
   for (int j = 0; j < n; ++j) {
     // first owned column > j
     int c = gw;
     if (c <= j) c += ((j - gw) / nw + 1) * nw;
     if (c >= ncol) break;  // nothing left for this warp
-    flag_wait(flags + j, 1);
+    flag_wait(flags + j, epoch);
     __syncwarp();
     const md::mdv<K> v0 = md::load_cg<K>(vhead, n, j);
     const md::mdv<K> bt = md::load_cg<K>(beta, n, j);
@@ -198,7 +204,7 @@ __global__ void __launch_bounds__(128) householder_qr_kernel(int n, const double
         x0 = md::shfl<K>(x0, (j + 1 - j) & 31);  // row j+1 lives in lane 1
         reflector_from_sigma<K>(n, j + 1, sig, x0, W, vhead, beta, rdiag, status);
         __syncwarp();
-        if (lane == 0) flag_set(flags + j + 1, 1);
+        if (lane == 0) flag_set(flags + j + 1, epoch);
       }
     }
   }

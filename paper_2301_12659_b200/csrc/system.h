@@ -48,7 +48,8 @@ struct ns_system {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double* A0q = nullptr;
-  int* qr_flags = nullptr;  // [n] reflector-ready flags of the QR kernel  // dense A_0 as factored (a0_kernel or ns_toeplitz_solve input)
+  int* qr_flags = nullptr;  // [n] reflector-ready flags of the QR kernel (epoch valued)
+  int qr_epoch = 0;  // dense A_0 as factored (a0_kernel or ns_toeplitz_solve input)
   int ledger_head = 0, ledger_count = 0;     // ring of steps whose events are not yet read
   ns_ledger ledger{};
   int last_launches = 0;
@@ -64,7 +65,7 @@ template <int K>
 struct Impl {
   static ns_status setup(ns_system* s);
   static ns_status evaldiff(ns_system* s, const double* x, cudaStream_t st);
-  static ns_status qr(ns_system* s, const double* A0src, cudaStream_t st);
+  static ns_status qr(ns_system* s, const double* A0src, const double* x, cudaStream_t st);
   static ns_status a0(ns_system* s, const double* x, cudaStream_t st);
   static ns_status stage(ns_system* s, int k_lo, cudaStream_t st);
   static ns_status residual(ns_system* s, double* x, double* res_out, cudaStream_t st);
