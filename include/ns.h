@@ -137,6 +137,9 @@ ns_status ns_md_op(int precision, int op, int n, const double* a, const double* 
  * every SM; writes the achieved rate in G instructions/s and the kernel time.
  * Synchronises the device (measurement entry, not part of the step). */
 ns_status ns_fp64_peak_probe(int device, int op, double* ginstr_per_s, double* ms);
+/* Cost of one grid barrier of the cooperative kernels (microseconds) for a
+ * grid of `blocks` x `threads`.  Synchronises. */
+ns_status ns_barrier_probe(int device, int blocks, int threads, double* us_per_barrier);
 /* Latency of one md operation in a dependent chain on one warp (SM cycles):
  * op 0 fused accumulate, 1 add, 2 mul, 3 reciprocal, 4 sqrt.  Synchronises. */
 ns_status ns_md_latency_probe(int precision, int op, double* cycles_per_op);

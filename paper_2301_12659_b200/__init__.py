@@ -32,7 +32,7 @@ EXPORTS = ["ns_system_create", "ns_system_destroy", "ns_newton_series_step",
            "ns_newton_series_step_batched", "ns_eval_diff", "ns_nnz", "ns_jacobian_pattern",
            "ns_toeplitz_solve", "ns_get_r_diag", "ns_md_op", "ns_get_status", "ns_get_ledger",
            "ns_reset_ledger", "ns_last_launch_count", "ns_strerror", "ns_build_info",
-           "ns_fp64_peak_probe", "ns_md_latency_probe"]
+           "ns_fp64_peak_probe", "ns_md_latency_probe", "ns_barrier_probe"]
 
 
 class NSError(RuntimeError):
@@ -95,6 +95,8 @@ def lib() -> ctypes.CDLL:
         "ns_fp64_peak_probe": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                 ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
         "ns_md_latency_probe": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+        "ns_barrier_probe": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)],
+                             ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -274,4 +276,11 @@ def md_latency_probe(precision: int, op: str = "fma") -> float:
     v = ctypes.c_double()
     code = {"fma": 0, "add": 1, "mul": 2, "recip": 3, "sqrt": 4}[op]
     _check(lib().ns_md_latency_probe(precision, code, ctypes.byref(v)), "ns_md_latency_probe")
+    return v.value
+
+
+def barrier_probe(blocks: int, threads: int = 128, device: int = 0) -> float:
+    """Microseconds per grid barrier of the cooperative kernels."""
+    v = ctypes.c_double()
+    _check(lib().ns_barrier_probe(device, blocks, threads, ctypes.byref(v)), "ns_barrier_probe")
     return v.value

@@ -12,6 +12,7 @@
 
 #include "../../include/ns.h"
 #include "system.h"
+#include "common.cuh"
 
 #define CK NS_CK
 #define dalloc ns_dalloc
@@ -539,4 +540,38 @@ extern "C" ns_status ns_md_latency_probe(int precision, int op, double* cycles_p
     case 8: return Impl<8>::latency(op, 256, cycles_per_op);
     default: return NS_EPREC;
   }
+}
+
+// ------------------------------------------------------------------ grid barrier probe
+namespace {
+__global__ void barrier_probe_kernel(int iters, unsigned* bar) {
+  for (int i = 0; i < iters; ++i) ns::grid_sync(bar);
+}
+}  // namespace
+
+extern "C" ns_status ns_barrier_probe(int device, int blocks, int threads, double* us_per_barrier) {
+  if (!us_per_barrier || blocks < 1 || threads < 32) return NS_EINVAL;
+  CK(cudaSetDevice(device));
+  unsigned* bar = nullptr;
+  CK(cudaMalloc(&bar, 2 * sizeof(unsigned)));
+  CK(cudaMemset(bar, 0, 2 * sizeof(unsigned)));
+  int iters = 8;
+  void* args[] = {&iters, &bar};
+  CK(cudaLaunchCooperativeKernel((const void*)barrier_probe_kernel, dim3(blocks), dim3(threads), args, 0, 0));
+  CK(cudaDeviceSynchronize());
+  iters = 2000;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0));
+  CK(cudaLaunchCooperativeKernel((const void*)barrier_probe_kernel, dim3(blocks), dim3(threads), args, 0, 0));
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(bar);
+  *us_per_barrier = ms * 1e3 / iters;
+  return NS_OK;
 }
