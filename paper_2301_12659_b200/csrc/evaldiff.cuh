@@ -25,14 +25,15 @@ namespace ns {
 struct SerRef {
   const double* p;  // coefficient 0 of limb plane 0
   long long ls;     // limb-plane stride
+  bool cg = false;  // written by another SM in this kernel: load through L2 (ld.global.cg)
 };
 
 // Batched truncated convolutions c_b = a_b * b_b (b = 0..B-1) by the threads
 // tid = 0..T-1 (a whole CTA, or one warp with T = 32).  get(bi, a, b, c)
 // returns the operands of convolution bi; outputs are compact series (limb
 // stride d).  T must be a multiple of 32 or equal to 32.
-template <int K, typename Get, bool CG = false>
-__device__ void conv_batch(int tid, int T, int B, int d, Get get) {
+template <int K, typename Get>
+__device__ void conv_batch(int tid, int T, int B, int d, Get get, double* const* c2 = nullptr) {
   const int P = (d + 1) / 2;
   const int groups = B * P;
   int G = 1;
@@ -50,12 +51,13 @@ __device__ void conv_batch(int tid, int T, int B, int d, Get get) {
     SerRef a, b;
     double* c;
     get(bi, a, b, c);
+#pragma unroll 2
     for (int t = sub; t < tot; t += G) {
       const bool first = t <= k1;
       const int k = first ? k1 : k2;
       const int j = first ? t : t - k1 - 1;
-      md::mdv<K> x = CG ? md::load_cg<K>(a.p, a.ls, j) : md::load<K>(a.p, a.ls, j);
-      md::mdv<K> y = CG ? md::load_cg<K>(b.p, b.ls, k - j) : md::load<K>(b.p, b.ls, k - j);
+      md::mdv<K> x = a.cg ? md::load_cg<K>(a.p, a.ls, j) : md::load<K>(a.p, a.ls, j);
+      md::mdv<K> y = b.cg ? md::load_cg<K>(b.p, b.ls, k - j) : md::load<K>(b.p, b.ls, k - j);
       md::mdv<K> cur;
 #pragma unroll
       for (int l = 0; l < K; ++l) cur.x[l] = first ? acc1.x[l] : acc2.x[l];
@@ -73,6 +75,10 @@ __device__ void conv_batch(int tid, int T, int B, int d, Get get) {
     if (active && sub == 0) {
       md::store<K>(c, d, k1, acc1);
       if (k2 != k1) md::store<K>(c, d, k2, acc2);
+      if (c2) {  // second copy (the chain's pool series next to its smem copy)
+        md::store_cg<K>(c2[bi], d, k1, acc1);
+        if (k2 != k1) md::store_cg<K>(c2[bi], d, k2, acc2);
+      }
     }
   }
 }
@@ -142,27 +148,26 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
       double* F = J.pool + J.ser_off[tau] * ser;  // F[q-1] = f_q
       double* G = F + (m - 1) * ser;              // G[q-1] = g_q
       double* X = G + (m - 2) * ser;              // X[j-2] = d/dx_j
-      if (jb.x == 0) {
-        for (int q = 1; q <= m - 1; ++q) {
+      if (jb.x <= 1) {
+        // chain: forward (f_q = f_{q-1} * x_{v(q+1)}) or backward (g_q = g_{q-1} * x_{v(m-q)});
+        // the running product stays in shared memory (double buffer), a copy goes
+        // to the pool for the cross jobs and the equation job.
+        const bool fwd = (jb.x == 0);
+        const int len = fwd ? m - 1 : m - 2;
+        double* base = fwd ? F : G;
+        double* sbuf[2] = {bacc + K * d, bacc + 2 * K * d};
+        for (int q = 1; q <= len; ++q) {
+          double* outp = base + (q - 1) * ser;
           auto get = [&](int, SerRef& pa, SerRef& pb, double*& pc) {
-            pa = (q == 1) ? SerRef{x + (long long)vars[0] * d, xs} : SerRef{F + (q - 2) * ser, d};
-            pb = SerRef{x + (long long)vars[q] * d, xs};
-            pc = F + (q - 1) * ser;
+            const int v0 = fwd ? vars[0] : vars[m - 1];
+            const int vq = fwd ? vars[q] : vars[m - 1 - q];
+            pa = (q == 1) ? SerRef{x + (long long)v0 * d, xs} : SerRef{sbuf[(q - 1) & 1], d};
+            pb = SerRef{x + (long long)vq * d, xs};
+            pc = sbuf[q & 1];
           };
-          conv_batch<K, decltype(get), true>(threadIdx.x, blockDim.x, 1, d, get);
+          conv_batch<K>(threadIdx.x, blockDim.x, 1, d, get, &outp);
           __syncthreads();
-          if (threadIdx.x == 0) publish(J.fprog + tau, q);
-        }
-      } else if (jb.x == 1) {
-        for (int q = 1; q <= m - 2; ++q) {
-          auto get = [&](int, SerRef& pa, SerRef& pb, double*& pc) {
-            pa = (q == 1) ? SerRef{x + (long long)vars[m - 1] * d, xs} : SerRef{G + (q - 2) * ser, d};
-            pb = SerRef{x + (long long)vars[m - 1 - q] * d, xs};
-            pc = G + (q - 1) * ser;
-          };
-          conv_batch<K, decltype(get), true>(threadIdx.x, blockDim.x, 1, d, get);
-          __syncthreads();
-          if (threadIdx.x == 0) publish(J.gprog + tau, q);
+          if (threadIdx.x == 0) publish(fwd ? J.fprog + tau : J.gprog + tau, q);
         }
       } else {
         const int j = jb.z;  // 2..m-1
@@ -172,12 +177,12 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
         }
         __syncthreads();
         auto get = [&](int, SerRef& pa, SerRef& pb, double*& pc) {
-          pa = (j - 2 == 0) ? SerRef{x + (long long)vars[0] * d, xs} : SerRef{F + (j - 3) * ser, d};
+          pa = (j - 2 == 0) ? SerRef{x + (long long)vars[0] * d, xs} : SerRef{F + (j - 3) * ser, d, true};
           const int gq = m - j - 1;
-          pb = (gq == 0) ? SerRef{x + (long long)vars[m - 1] * d, xs} : SerRef{G + (gq - 1) * ser, d};
+          pb = (gq == 0) ? SerRef{x + (long long)vars[m - 1] * d, xs} : SerRef{G + (gq - 1) * ser, d, true};
           pc = X + (j - 2) * ser;
         };
-        conv_batch<K, decltype(get), true>(threadIdx.x, blockDim.x, 1, d, get);
+        conv_batch<K>(threadIdx.x, blockDim.x, 1, d, get);
         __syncthreads();
       }
       if (threadIdx.x == 0) {

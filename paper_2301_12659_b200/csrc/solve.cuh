@@ -169,25 +169,47 @@ __global__ void __launch_bounds__(128) householder_qr_kernel(DevSys sy, const do
     sig = md::group_sum<K>(sig, 32);
     reflector_from_sigma<K>(n, 0, sig, md::load_cg<K>(W, ls, 0), W, vhead, beta, rdiag, status);
     __syncwarp();
-    if (lane == 0) flag_set(flags + 0, epoch);
+    if (lane == 0) flag_set(flags + n, epoch);  // B[0]
   }
+  // Two flags per column j (epoch valued): A[j] = column j final below the
+  // diagonal (rows > j), B[j] = reflector j (vhead, beta) published.  After A[j]
+  // every warp forms the partial dot sum_{r>j} v_r W[r][c] of its columns while
+  // the owner of column j is still computing the norm, sqrt and reciprocal;
+  // after B[j] it adds v0 W[j][c] and applies the update.
+  int* fA = flags;
+  int* fB = flags + n;
   for (int j = 0; j < n; ++j) {
     // first owned column > j
-    int c = gw;
-    if (c <= j) c += ((j - gw) / nw + 1) * nw;
-    if (c >= ncol) break;  // nothing left for this warp
-    flag_wait(flags + j, epoch);
+    int c0 = gw;
+    if (c0 <= j) c0 += ((j - gw) / nw + 1) * nw;
+    if (c0 >= ncol) break;  // nothing left for this warp
+    if (j > 0) flag_wait(fA + j, epoch);  // column 0 was final at the start
+    __syncwarp();
+    constexpr int MAXC = 4;  // columns per warp kept in flight (ncol <= 4 nw)
+    md::mdv<K> part[MAXC];
+    int nc = 0;
+    for (int c = c0; c < ncol && nc < MAXC; c += nw, ++nc) {
+      md::mdv<K> p = md::zero<K>();
+      for (int r = j + 1 + lane; r < n; r += 32)
+        p = md::fma_acc<K>(p, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)c * n + r));
+      part[nc] = md::group_sum<K>(p, 32);
+    }
+    flag_wait(fB + j, epoch);
     __syncwarp();
     const md::mdv<K> v0 = md::load_cg<K>(vhead, n, j);
     const md::mdv<K> bt = md::load_cg<K>(beta, n, j);
-    for (; c < ncol; c += nw) {
-      // column c -= beta_j v (v^T column c), rows j..n-1
-      md::mdv<K> dot = md::zero<K>();
-      for (int r = j + lane; r < n; r += 32) {
-        const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
-        dot = md::fma_acc<K>(dot, v, md::load_cg<K>(W, ls, (long long)c * n + r));
+    int ic = 0;
+    for (int c = c0; c < ncol; c += nw, ++ic) {
+      md::mdv<K> dot;
+      if (ic < MAXC) {
+        dot = part[ic];
+      } else {  // more columns than kept in flight: full dot here
+        md::mdv<K> p = md::zero<K>();
+        for (int r = j + 1 + lane; r < n; r += 32)
+          p = md::fma_acc<K>(p, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)c * n + r));
+        dot = md::group_sum<K>(p, 32);
       }
-      dot = md::group_sum<K>(dot, 32);
+      dot = md::fma_acc<K>(dot, v0, md::load_cg<K>(W, ls, (long long)c * n + j));
       const md::mdv<K> nw_ = md::neg<K>(md::mul<K>(bt, dot));
       const bool look = (c == j + 1 && c < n);
       md::mdv<K> sig = md::zero<K>(), x0 = md::zero<K>();
@@ -199,12 +221,13 @@ __global__ void __launch_bounds__(128) householder_qr_kernel(DevSys sy, const do
         if (r == j + 1) x0 = w;
       }
       if (look) {
-        // rows j+1..n-1 of the updated column are the next reflector's x
+        __syncwarp();
+        if (lane == 0) flag_set(fA + j + 1, epoch);  // column j+1 final below its diagonal
         sig = md::group_sum<K>(sig, 32);
-        x0 = md::shfl<K>(x0, (j + 1 - j) & 31);  // row j+1 lives in lane 1
+        x0 = md::shfl<K>(x0, 1);  // row j+1 lives in lane 1
         reflector_from_sigma<K>(n, j + 1, sig, x0, W, vhead, beta, rdiag, status);
         __syncwarp();
-        if (lane == 0) flag_set(flags + j + 1, epoch);
+        if (lane == 0) flag_set(fB + j + 1, epoch);
       }
     }
   }
@@ -314,6 +337,7 @@ __global__ void __launch_bounds__(128) form_m_kernel(int n, int TB, const double
       const int r = t0 + w / jg, j = (w % jg) * 32 + lane;
       if (j < n) {
         md::mdv<K> acc = md::load<K>(Qt, lsM, (long long)r * n + j);
+#pragma unroll 4
         for (int c = t1; c < n; ++c)
           acc = md::fma_acc<K>(acc, md::neg<K>(md::load<K>(R, lsM, (long long)r * n + c)),
                                md::load_cg<K>(M, lsM, (long long)c * n + j));
@@ -325,6 +349,7 @@ __global__ void __launch_bounds__(128) form_m_kernel(int n, int TB, const double
       const int r = t0 + w / jg, j = (w % jg) * 32 + lane;
       if (j < n) {
         md::mdv<K> acc = md::zero<K>();
+#pragma unroll 4
         for (int c = t0; c < t1; ++c)
           acc = md::fma_acc<K>(acc, md::load<K>(invR, lsI, (long long)t * TB * TB + (long long)(r - t0) * TB + (c - t0)),
                                md::load_cg<K>(Z, lsM, (long long)c * n + j));
