@@ -31,25 +31,39 @@ struct DevSys {
   const double* rhs;    // [K][n][d]
 };
 
-// Sense-reversing grid barrier for a cooperative (co-resident) launch.
-// bar[0] = arrival count, bar[1] = generation.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned atom_add_acqrel_u32(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Grid barrier for a cooperative (co-resident) launch: bar[0] = arrival count,
+// bar[1] = generation.  The CTA's writes are ordered before the arrival by
+// __syncthreads + the acq_rel atomic; waiters spin on an acquire load of the
+// generation (no sleep: the wait is short and latency matters).
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    const unsigned gen = *vgen;
     const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == nb - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
+    const unsigned gen = ld_acquire_u32(bar + 1);
+    if (atom_add_acqrel_u32(bar, 1u) == nb - 1) {
+      st_relaxed_u32(bar, 0u);
+      st_release_u32(bar + 1, gen + 1);
     } else {
-      while (*vgen == gen) {
-        __nanosleep(32);
+      while (ld_acquire_u32(bar + 1) == gen) {
       }
     }
-    __threadfence();
   }
   __syncthreads();
 }

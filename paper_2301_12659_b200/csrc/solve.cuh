@@ -113,17 +113,16 @@ __device__ void reflector_from_sigma(int n, int jj, const md::mdv<K>& sig, const
 }
 
 __device__ __forceinline__ void flag_wait(const int* f, int v) {
-  int ns = 16;
   for (;;) {
     int cur;
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(cur) : "l"(f) : "memory");
     if (cur >= v) break;
-    __nanosleep(ns);
-    ns = min(ns * 2, 256);
   }
 }
+// all lanes' prior writes are ordered by the caller's __syncwarp; the release
+// store (after an acq_rel fence, cumulative) publishes them
 __device__ __forceinline__ void flag_set(int* f, int v) {
-  __threadfence();
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
 }
 
