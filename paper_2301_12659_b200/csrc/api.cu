@@ -545,7 +545,8 @@ extern "C" ns_status ns_md_latency_probe(int precision, int op, double* cycles_p
 // ------------------------------------------------------------------ grid barrier probe
 namespace {
 __global__ void barrier_probe_kernel(int iters, unsigned* bar) {
-  for (int i = 0; i < iters; ++i) ns::grid_sync(bar);
+  ns::GridBarrier gb(bar, 0u);
+  for (int i = 0; i < iters; ++i) gb.sync();
 }
 }  // namespace
 
@@ -560,6 +561,7 @@ extern "C" ns_status ns_barrier_probe(int device, int blocks, int threads, doubl
   CK(cudaLaunchCooperativeKernel((const void*)barrier_probe_kernel, dim3(blocks), dim3(threads), args, 0, 0));
   CK(cudaDeviceSynchronize());
   iters = 2000;
+  CK(cudaMemset(bar, 0, 2 * sizeof(unsigned)));
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));

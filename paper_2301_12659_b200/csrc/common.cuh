@@ -48,11 +48,31 @@ __device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Grid barrier for a cooperative (co-resident) launch: bar[0] = arrival count,
-// bar[1] = generation.  The CTA's writes are ordered before the arrival by
-// __syncthreads + the acq_rel atomic; waiters spin on an acquire load of the
-// generation (no sleep: the wait is short and latency matters).
+// Grid barrier for a cooperative (co-resident) launch on a monotonic arrival
+// counter: barrier i of a launch completes when the counter reaches
+// base + i * gridDim.  Each CTA adds 1 with a fire-and-forget release
+// reduction and spins on an acquire load: one L2 round trip after the last
+// arrival.  The counter is zeroed before the launch (base 0) or, for a kernel
+// launched without a memset, advanced by a known amount per launch (base).
+struct GridBarrier {
+  unsigned* cnt;
+  unsigned target;
+  __device__ __forceinline__ GridBarrier(unsigned* c, unsigned base) : cnt(c), target(base) {}
+  __device__ __forceinline__ void sync() {
+    __syncthreads();
+    target += gridDim.x * gridDim.y * gridDim.z;
+    if (threadIdx.x == 0) {
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+      while ((int)(ld_acquire_u32(cnt) - target) < 0) {
+      }
+    }
+    __syncthreads();
+  }
+};
+
+// single-use form (counter zeroed before the launch, barriers counted by the caller)
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
+  // bar[1] holds this CTA-independent barrier index; bar[0] the arrival counter
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned nb = gridDim.x * gridDim.y * gridDim.z;

@@ -51,24 +51,21 @@ __device__ void conv_batch(int tid, int T, int B, int d, Get get, double* const*
     SerRef a, b;
     double* c;
     get(bi, a, b, c);
-    // terms of coefficient k1 (j = 0..k1) and of k2 (j = 0..k2) as two
-    // independent accumulation chains (ILP); lane `sub` takes every G-th term of
-    // the concatenated list, as before
-    const int n1 = active ? k1 + 1 : 0;
-#pragma unroll 2
-    for (int t = sub; t < n1; t += G) {
-      const md::mdv<K> xa = a.cg ? md::load_cg<K>(a.p, a.ls, t) : md::load<K>(a.p, a.ls, t);
-      const md::mdv<K> yb = b.cg ? md::load_cg<K>(b.p, b.ls, k1 - t) : md::load<K>(b.p, b.ls, k1 - t);
-      acc1 = md::fma_acc<K>(acc1, xa, yb);
-    }
-    // first index of the k2 part for this lane: smallest t >= n1 with t = sub (mod G)
-    const int t2 = n1 + ((sub - n1 % G) + G) % G;
-#pragma unroll 2
-    for (int t = t2; t < tot; t += G) {
-      const int j = t - n1;
-      const md::mdv<K> xa = a.cg ? md::load_cg<K>(a.p, a.ls, j) : md::load<K>(a.p, a.ls, j);
-      const md::mdv<K> yb = b.cg ? md::load_cg<K>(b.p, b.ls, k2 - j) : md::load<K>(b.p, b.ls, k2 - j);
-      acc2 = md::fma_acc<K>(acc2, xa, yb);
+    for (int t = sub; t < tot; t += G) {
+      const bool first = t <= k1;
+      const int k = first ? k1 : k2;
+      const int j = first ? t : t - k1 - 1;
+      md::mdv<K> xa = a.cg ? md::load_cg<K>(a.p, a.ls, j) : md::load<K>(a.p, a.ls, j);
+      md::mdv<K> yb = b.cg ? md::load_cg<K>(b.p, b.ls, k - j) : md::load<K>(b.p, b.ls, k - j);
+      md::mdv<K> cur;
+#pragma unroll
+      for (int l = 0; l < K; ++l) cur.x[l] = first ? acc1.x[l] : acc2.x[l];
+      cur = md::fma_acc<K>(cur, xa, yb);
+#pragma unroll
+      for (int l = 0; l < K; ++l) {
+        acc1.x[l] = first ? cur.x[l] : acc1.x[l];
+        acc2.x[l] = first ? acc2.x[l] : cur.x[l];
+      }
     }
     if (G > 1) {
       acc1 = md::group_sum<K>(acc1, G);

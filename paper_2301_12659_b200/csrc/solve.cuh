@@ -158,7 +158,10 @@ __global__ void __launch_bounds__(128) householder_qr_kernel(DevSys sy, const do
   }
   if (x)
     for (int i = gw; i < n; i += nw) a0_row<K>(sy, x, i, W, ls, 1, n);
-  grid_sync(bar);
+  {
+    GridBarrier gb(bar, (unsigned)(epoch - 1) * (gridDim.x * gridDim.y * gridDim.z));
+    gb.sync();
+  }
   if (gw == 0) {  // reflector 0 (owner of column 0)
     md::mdv<K> sig = md::zero<K>();
     for (int r = lane; r < n; r += 32) {
@@ -326,6 +329,7 @@ template <int K>
 __global__ void __launch_bounds__(128) form_m_kernel(int n, int TB, const double* __restrict__ R,
                                                      const double* __restrict__ Qt, const double* __restrict__ invR,
                                                      double* M, double* Z, unsigned* bar) {
+  GridBarrier gb(bar, 0u);
   const int gw = gwarp(), nw = nwarps(), lane = lane_id();
   const int T = (n + TB - 1) / TB;
   const long long lsM = (long long)n * n, lsI = (long long)T * TB * TB;
@@ -343,7 +347,7 @@ __global__ void __launch_bounds__(128) form_m_kernel(int n, int TB, const double
         md::store_cg<K>(Z, lsM, (long long)r * n + j, acc);
       }
     }
-    grid_sync(bar);
+    gb.sync();
     for (int w = gw; w < (t1 - t0) * jg; w += nw) {
       const int r = t0 + w / jg, j = (w % jg) * 32 + lane;
       if (j < n) {
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(128) form_m_kernel(int n, int TB, const double
         md::store_cg<K>(M, lsM, (long long)r * n + j, acc);
       }
     }
-    grid_sync(bar);
+    gb.sync();
   }
 }
 
@@ -380,6 +384,7 @@ constexpr int UCH = 64;  // update terms per chunk (32 lanes x 2)
 
 template <int K>
 __global__ void __launch_bounds__(128) stage_kernel(DevSys s, StageArgs a, unsigned* bar) {
+  GridBarrier gb(bar, 0u);
   const int n = s.n, d = s.d, nnz = s.nnz;
   const int gw = gwarp(), nw = nwarps(), lane = lane_id();
   const long long lsV = (long long)d * n;     // limb stride of [K][d][n]
@@ -418,7 +423,7 @@ __global__ void __launch_bounds__(128) stage_kernel(DevSys s, StageArgs a, unsig
         acc = md::group_sum<K>(acc, 32);
         if (lane == 0) md::store_cg<K>(a.part, lsP, (long long)i * a.cmax + c, acc);
       }
-      grid_sync(bar);
+      gb.sync();
       for (int i = gw; i < n; i += nw) {
         const int len = s.row_ptr[i + 1] - s.row_ptr[i];
         const int nc = (kk * len + UCH - 1) / UCH;
@@ -434,7 +439,7 @@ __global__ void __launch_bounds__(128) stage_kernel(DevSys s, StageArgs a, unsig
       for (int i = gw; i < n; i += nw)
         if (lane == 0) md::store_cg<K>(a.bp + (long long)k * n, lsV, i, md::load<K>(a.b + (long long)k * n, lsV, i));
     }
-    grid_sync(bar);
+    gb.sync();
     if (a.M) {
       // ---- dx_k = M b'_k  (qhb and bs in one matvec)
       for (int i = gw; i < n; i += nw) {
@@ -445,7 +450,7 @@ __global__ void __launch_bounds__(128) stage_kernel(DevSys s, StageArgs a, unsig
         acc = md::group_sum<K>(acc, 32);
         if (lane == 0) md::store_cg<K>(a.dx + (long long)k * n, lsV, i, acc);
       }
-      grid_sync(bar);
+      gb.sync();
       continue;
     }
     // ---- qhb: y = Q^T b'_k
@@ -459,7 +464,7 @@ __global__ void __launch_bounds__(128) stage_kernel(DevSys s, StageArgs a, unsig
       acc = md::group_sum<K>(acc, 32);
       if (lane == 0) md::store_cg<K>(a.y, n, i, acc);
     }
-    grid_sync(bar);
+    gb.sync();
     // ---- bs: tiles last to first
     for (int t = T - 1; t >= 0; --t) {
       const int t0 = t * TB, t1 = min(n, t0 + TB);
@@ -478,7 +483,7 @@ __global__ void __launch_bounds__(128) stage_kernel(DevSys s, StageArgs a, unsig
             md::store_cg<K>(a.y, n, r, md::sub<K>(yr, acc));
           }
         }
-        grid_sync(bar);
+        gb.sync();
       }
       // dx_k[r] = sum_{c in tile} invR_t[r][c] z_c
       for (int r = t0 + gw; r < t1; r += nw) {
@@ -491,7 +496,7 @@ __global__ void __launch_bounds__(128) stage_kernel(DevSys s, StageArgs a, unsig
         acc = md::group_sum<K>(acc, 32);
         if (lane == 0) md::store_cg<K>(a.dx + (long long)k * n, lsV, r, acc);
       }
-      grid_sync(bar);
+      gb.sync();
     }
   }
 }
