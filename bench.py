@@ -38,7 +38,8 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C5"])
+    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    p.add_argument("--reuse-qr", action="store_true", help="C4: NS_REUSE_QR in the timed steps (QR once)")
     p.add_argument("--batch", type=int, default=4096, help="C5: total paths (partitioned over ranks)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
@@ -317,6 +318,94 @@ def run_c5(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------ C4: one large system, sharded eval/diff
+def run_c4(args):
+    """BASELINE configs[3]: dim 1024 2-column banded (w = 32) system, degree 31,
+    quad double.  Equation-owner sharding of eval/diff over the ranks
+    (dist.equation_partition), row replication by all-gather over NVLink
+    (torch.distributed NCCL), then the QR + stage loop + residual replicated on
+    every rank (ns_newton_series_step_from).  Strong scaling (one system)."""
+    import numpy as np
+    import torch
+
+    import paper_2301_12659_b200 as P
+    import synth
+    from paper_2301_12659_b200 import perfmodel as PM
+    from paper_2301_12659_b200.dist import equation_partition, max_over_ranks, replicate_rows
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    sys_ = synth.build_config("C4")
+    x_np = synth.make_x(sys_, "near", seed=1)
+    dev = torch.device(f"cuda:{local}")
+    h = P.NewtonSystem.from_system(sys_, device=local)
+    ranges = equation_partition(sys_.eq_ptr, sys_.mono_ptr, sys_.d, ws)
+    lo, hi = ranges[rank]
+    if ws > 1:
+        h.set_partition(lo, hi)
+    rp, _ = h.pattern()
+    x0 = torch.tensor(x_np, device=dev)
+    x = x0.clone()
+    res = torch.zeros((4, 3), dtype=torch.float64, device=dev)
+    c, per_class, total = work(sys_, h.nnz)
+    flops_step = PM.flops(total, sys_.K)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def one(flags):
+        b, A, A0 = h.eval_diff(x)
+        replicate_rows(b, A, A0, rp, ranges, rank)
+        h.step_from(x, b, A, A0, res, flags=flags)
+
+    for _ in range(max(args.warmup, 3)):
+        x.copy_(x0)
+        one(0)
+    torch.cuda.synchronize()
+    flags = P.NS_REUSE_QR if args.reuse_qr else 0
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        x.copy_(x0)
+        flush.zero_()
+        ev[i][0].record(stream)
+        one(flags)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms_total = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev), dev)
+    ms_step = ms_total / args.steps
+    probe = P.fp64_peak_probe(local, "dfma")
+    peak = 2.0 * probe["ginstr_per_s"]
+    fl = flops_step - (PM.flops(per_class["qr"], sys_.K) if args.reuse_qr else 0)
+    value = fl / (ms_step * 1e-3) * 1e-9
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded, synth.py; 'near' start series)",
+        "config": {"workload": "C4: dim=1024 2-column banded (w=32) monomial system, degree 31, quad double, "
+                               "eval/diff sharded by equations + all-gather row replication, solve replicated",
+                   "ranges": ranges, "reuse_qr": bool(args.reuse_qr),
+                   "l2": "flushed (256 MiB memset) before every timed step"},
+        "pct_of_peak": 100.0 * value / (ws * peak),
+        "roofline": {"bound": "alu", "achieved": value, "peak": peak, "unit": "GFLOP/s", "frac": value / peak,
+                     "traffic": None, "peak_source": "measured DFMA-chain probe x2"},
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     import numpy as np
@@ -464,6 +553,8 @@ def main():
         run_reference(args)
     elif args.config == "C5":
         run_c5(args)
+    elif args.config == "C4":
+        run_c4(args)
     else:
         run_ours(args)
 

@@ -116,6 +116,19 @@ ns_status ns_newton_series_step_batched(ns_system* sys, int precision, int dim, 
                                         double* x_series, const double* rhs, double* residual_out,
                                         uint32_t flags, void* stream);
 
+/* Sharded eval/diff: after ns_set_partition(sys, lo, hi) the
+ * eval/diff of this handle (ns_eval_diff) computes only the rows [lo, hi) of b,
+ * A and A0 (equation-owner sharding; the other rows are left untouched).  The
+ * caller replicates the rows across ranks (all-gather over NVLink) and runs
+ * ns_newton_series_step_from on every rank.  NS_EINVAL for an empty or
+ * out-of-range partition; synchronises the handle's device. */
+ns_status ns_set_partition(ns_system* sys, int eq_lo, int eq_hi);
+/* The step after eval/diff: QR of the given A0, stage loop, residual and
+ * x += dx, for (b, A, A0) computed elsewhere (all device, layouts as above). */
+ns_status ns_newton_series_step_from(ns_system* sys, int precision, int dim, int degree, double* x_series,
+                                     const double* b, const double* A, const double* A0,
+                                     double* residual_out, uint32_t flags, void* stream);
+
 /* Parity/debug entry points: the same kernels as the step. */
 /* eval/diff only: b [K][d][n], A [K][d][nnz], A0 [K][n][n], all device */
 ns_status ns_eval_diff(ns_system* sys, const double* x_series, double* b, double* A, double* A0,

@@ -32,7 +32,8 @@ EXPORTS = ["ns_system_create", "ns_system_destroy", "ns_newton_series_step",
            "ns_newton_series_step_batched", "ns_eval_diff", "ns_nnz", "ns_jacobian_pattern",
            "ns_toeplitz_solve", "ns_get_r_diag", "ns_md_op", "ns_get_status", "ns_get_ledger",
            "ns_reset_ledger", "ns_last_launch_count", "ns_strerror", "ns_build_info",
-           "ns_fp64_peak_probe", "ns_md_latency_probe", "ns_barrier_probe"]
+           "ns_fp64_peak_probe", "ns_md_latency_probe", "ns_barrier_probe", "ns_set_partition",
+           "ns_newton_series_step_from"]
 
 
 class NSError(RuntimeError):
@@ -81,6 +82,9 @@ def lib() -> ctypes.CDLL:
         "ns_newton_series_step_batched": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp,
                                            u32, vp], ctypes.c_int),
         "ns_eval_diff": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
+        "ns_set_partition": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+        "ns_newton_series_step_from": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, u32, vp],
+                                       ctypes.c_int),
         "ns_nnz": ([vp], i32),
         "ns_jacobian_pattern": ([vp, vp, vp], ctypes.c_int),
         "ns_toeplitz_solve": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
@@ -194,6 +198,23 @@ class NewtonSystem:
         _check(lib().ns_newton_series_step_batched(self._h, self.K, self.n, self.D, B, _ptr(x), _ptr(rhs),
                                                    _ptr(residual_out), flags, _stream_ptr(stream)),
                "ns_newton_series_step_batched")
+
+    # ---- sharded eval/diff (C4)
+    def set_partition(self, eq_lo: int, eq_hi: int):
+        """ns_set_partition: this handle's eval/diff computes rows [eq_lo, eq_hi)."""
+        _check(lib().ns_set_partition(self._h, eq_lo, eq_hi), "ns_set_partition")
+
+    def step_from(self, x, b, A, A0, residual_out=None, flags: int = 0, stream=None):
+        """ns_newton_series_step_from: QR + stage loop + residual + x += dx for given (b, A, A0)."""
+        _require_cuda(x, "x", (self.K, self.n, self.d))
+        _require_cuda(b, "b", (self.K, self.d, self.n))
+        _require_cuda(A, "A", (self.K, self.d, self.nnz))
+        _require_cuda(A0, "A0", (self.K, self.n, self.n))
+        if residual_out is not None:
+            _require_cuda(residual_out, "residual_out", (self.K, 3))
+        _check(lib().ns_newton_series_step_from(self._h, self.K, self.n, self.D, _ptr(x), _ptr(b), _ptr(A),
+                                                _ptr(A0), _ptr(residual_out), flags, _stream_ptr(stream)),
+               "ns_newton_series_step_from")
 
     # ---- debug / parity entry points
     def eval_diff(self, x, stream=None):

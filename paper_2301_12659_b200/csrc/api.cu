@@ -122,6 +122,42 @@ void free_all(ns_system* s) {
   if (s->side) cudaStreamDestroy(s->side);
 }
 
+// Job list of the eval/diff job queue for the equations [eq_lo, eq_hi): chains
+// longest first (LPT), cross products by the layer their inputs appear at,
+// equations by their longest monomial.  ser_off / left cover all monomials.
+void build_jobs(const ns_system* s, int eq_lo, int eq_hi, std::vector<int4>& jobs, std::vector<long long>& ser_off,
+                std::vector<int>& left, long long& pool_series) {
+  const int M = s->M;
+  std::vector<int4> chains, cross, eqs;
+  ser_off.assign(M, 0);
+  left.assign(M, 0);
+  pool_series = 0;
+  auto prod = [](int m) { return m <= 1 ? 0 : (m == 2 ? 1 : 3 * m - 5); };
+  for (int t = 0; t < M; ++t) {
+    const int m = s->h_mono_ptr[t + 1] - s->h_mono_ptr[t];
+    ser_off[t] = pool_series;
+    pool_series += prod(m);
+    left[t] = (m <= 1) ? 0 : (m == 2 ? 1 : m);
+  }
+  for (int i = eq_lo; i < eq_hi; ++i) {
+    int mm = 0;
+    for (int t = s->h_eq_ptr[i]; t < s->h_eq_ptr[i + 1]; ++t) {
+      const int m = s->h_mono_ptr[t + 1] - s->h_mono_ptr[t];
+      mm = std::max(mm, m);
+      if (m >= 2) chains.push_back(make_int4(0, t, m - 1, 0));
+      if (m >= 3) chains.push_back(make_int4(1, t, m - 2, 0));
+      for (int j = 2; j <= m - 1; ++j) cross.push_back(make_int4(2, t, j, std::max(j - 2, m - j - 1)));
+    }
+    eqs.push_back(make_int4(3, i, 0, mm));
+  }
+  std::stable_sort(chains.begin(), chains.end(), [](int4 a, int4 b) { return a.z > b.z; });
+  std::stable_sort(cross.begin(), cross.end(), [](int4 a, int4 b) { return a.w < b.w; });
+  std::stable_sort(eqs.begin(), eqs.end(), [](int4 a, int4 b) { return a.w < b.w; });
+  jobs = chains;
+  jobs.insert(jobs.end(), cross.begin(), cross.end());
+  jobs.insert(jobs.end(), eqs.begin(), eqs.end());
+}
+
 }  // namespace
 
 
@@ -211,34 +247,14 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   std::stable_sort(s->h_job_order.begin(), s->h_job_order.end(),
                    [&](int a, int b) { return cost[a] > cost[b]; });
 
-  // eval/diff job queue (see evaldiff.cuh): chains longest first, cross products by
-  // the layer their inputs appear at, equations by their longest monomial
-  std::vector<int4> chains, cross, eqs;
-  std::vector<long long> ser_off(M, 0);
-  std::vector<int> left(M, 0);
+  // eval/diff job queue (see evaldiff.cuh)
+  std::vector<int4> jobs;
+  std::vector<long long> ser_off;
+  std::vector<int> left;
   long long pool_series = 0;
-  auto prod = [](int m) { return m <= 1 ? 0 : (m == 2 ? 1 : 3 * m - 5); };
-  for (int t = 0; t < M; ++t) {
-    const int m = s->h_mono_ptr[t + 1] - s->h_mono_ptr[t];
-    ser_off[t] = pool_series;
-    pool_series += prod(m);
-    if (m >= 2) chains.push_back(make_int4(0, t, m - 1, 0));
-    if (m >= 3) chains.push_back(make_int4(1, t, m - 2, 0));
-    for (int j = 2; j <= m - 1; ++j) cross.push_back(make_int4(2, t, j, std::max(j - 2, m - j - 1)));
-    left[t] = (m <= 1) ? 0 : (m == 2 ? 1 : m);
-  }
-  for (int i = 0; i < n; ++i) {
-    int mm = 0;
-    for (int t = s->h_eq_ptr[i]; t < s->h_eq_ptr[i + 1]; ++t) mm = std::max(mm, s->h_mono_ptr[t + 1] - s->h_mono_ptr[t]);
-    eqs.push_back(make_int4(3, i, 0, mm));
-  }
-  std::stable_sort(chains.begin(), chains.end(), [](int4 a, int4 b) { return a.z > b.z; });
-  std::stable_sort(cross.begin(), cross.end(), [](int4 a, int4 b) { return a.w < b.w; });
-  std::stable_sort(eqs.begin(), eqs.end(), [](int4 a, int4 b) { return a.w < b.w; });
-  std::vector<int4> jobs(chains);
-  jobs.insert(jobs.end(), cross.begin(), cross.end());
-  jobs.insert(jobs.end(), eqs.begin(), eqs.end());
+  build_jobs(s, 0, n, jobs, ser_off, left, pool_series);
   s->njobs = (int)jobs.size();
+  s->njobs_full = s->njobs;
 
   ns_status st = NS_OK;
   auto fail = [&](ns_status e) {
@@ -398,6 +414,59 @@ ns_status ns_eval_diff(ns_system* s, const double* x, double* b, double* A, doub
 }
 
 int32_t ns_nnz(const ns_system* s) { return s ? s->nnz : -1; }
+
+ns_status ns_set_partition(ns_system* s, int eq_lo, int eq_hi) {
+  if (!s || eq_lo < 0 || eq_hi > s->n || eq_lo >= eq_hi) return NS_EINVAL;
+  std::vector<int4> jobs;
+  std::vector<long long> ser_off;
+  std::vector<int> left;
+  long long pool_series = 0;
+  build_jobs(s, eq_lo, eq_hi, jobs, ser_off, left, pool_series);
+  CK(cudaSetDevice(s->dev));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(s->jobs, jobs.data(), sizeof(int4) * jobs.size(), cudaMemcpyHostToDevice));
+  s->njobs = (int)jobs.size();
+  s->eq_lo = eq_lo;
+  s->eq_hi = eq_hi;
+  return NS_OK;
+}
+
+ns_status ns_newton_series_step_from(ns_system* s, int precision, int dim, int degree, double* x, const double* b,
+                                     const double* A, const double* A0, double* res_out, uint32_t flags,
+                                     void* stream) {
+  if (!s || !x || !b || !A || !A0) return NS_EINVAL;
+  if (precision != s->K) return NS_EPREC;
+  if (dim != s->n || degree != s->D) return NS_EDIM;
+  if (flags & ~(NS_REUSE_QR | NS_NO_RESIDUAL | NS_LEDGER | NS_TILED_BS)) return NS_EINVAL;
+  if ((flags & NS_REUSE_QR) && !s->qr_cached) return NS_ESTATE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t K = s->K, d = s->d, n = s->n;
+  s->last_launches = 0;
+  CK(cudaMemcpyAsync(s->b, b, sizeof(double) * K * d * n, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(s->A, A, sizeof(double) * K * d * s->nnz, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(s->A0, A0, sizeof(double) * K * n * n, cudaMemcpyDeviceToDevice, st));
+  if (!(flags & NS_REUSE_QR)) s->use_m = !(flags & NS_TILED_BS);
+  ns_status r = NS_OK;
+  switch (s->K) {
+    case 2:
+      if (!(flags & NS_REUSE_QR)) r = Impl<2>::qr(s, s->A0, nullptr, st);
+      if (!r) r = Impl<2>::stage(s, 0, st);
+      if (!r) r = Impl<2>::residual(s, x, res_out, st);
+      break;
+    case 4:
+      if (!(flags & NS_REUSE_QR)) r = Impl<4>::qr(s, s->A0, nullptr, st);
+      if (!r) r = Impl<4>::stage(s, 0, st);
+      if (!r) r = Impl<4>::residual(s, x, res_out, st);
+      break;
+    default:
+      if (!(flags & NS_REUSE_QR)) r = Impl<8>::qr(s, s->A0, nullptr, st);
+      if (!r) r = Impl<8>::stage(s, 0, st);
+      if (!r) r = Impl<8>::residual(s, x, res_out, st);
+      break;
+  }
+  s->last_stream = st;
+  return r;
+}
 
 ns_status ns_jacobian_pattern(const ns_system* s, int32_t* row_ptr, int32_t* col_idx) {
   if (!s || !row_ptr || !col_idx) return NS_EINVAL;

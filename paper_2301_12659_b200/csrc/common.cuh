@@ -36,6 +36,21 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// relaxed (strong, no L1 invalidation) load for spin loops; an acquire fence is
+// issued once after the awaited value is seen (an ld.acquire in the loop emits
+// CCTL.IVALL on every iteration)
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned atom_add_acqrel_u32(unsigned* p, unsigned v) {
   unsigned old;
   asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
@@ -63,8 +78,9 @@ struct GridBarrier {
     target += gridDim.x * gridDim.y * gridDim.z;
     if (threadIdx.x == 0) {
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
-      while ((int)(ld_acquire_u32(cnt) - target) < 0) {
+      while ((int)(ld_relaxed_u32(cnt) - target) < 0) {
       }
+      fence_acq_rel();
     }
     __syncthreads();
   }

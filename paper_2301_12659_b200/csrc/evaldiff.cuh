@@ -111,10 +111,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 }
 __device__ __forceinline__ void wait_geq(const int* p, int v) {
   int ns = 32;
-  while (ld_acquire(p) < v) {
+  while (ld_relaxed_s32(p) < v) {
     __nanosleep(ns);
-    ns = min(ns * 2, 1024);
+    ns = min(ns * 2, 512);
   }
+  fence_acq_rel();
 }
 __device__ __forceinline__ void publish(int* p, int v) {
   __threadfence();
@@ -196,10 +197,11 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
     if (threadIdx.x == 0)
       for (int tau = s.eq_ptr[i]; tau < s.eq_ptr[i + 1]; ++tau) {
         int ns = 32;
-        while (ld_acquire(J.left + tau) > 0) {
+        while (ld_relaxed_s32(J.left + tau) > 0) {
           __nanosleep(ns);
-          ns = min(ns * 2, 1024);
+          ns = min(ns * 2, 512);
         }
+        fence_acq_rel();
       }
     for (int t = threadIdx.x; t < K * d; t += blockDim.x) {
       const int l = t / d, k = t % d;

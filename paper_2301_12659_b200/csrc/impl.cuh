@@ -138,7 +138,7 @@ ns_status setup_grids(ns_system* s) {
   s->ed_smem = 3 * sizeof(double) * (size_t)K * s->d;  // b accumulator + chain double buffer
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::evaldiff_jobs_kernel<K>, 256, s->ed_smem));
   if (occ < 1) return NS_ECUDA;
-  s->grid_ed = std::min(s->njobs, occ * s->sms);
+  s->grid_ed = std::min(s->njobs_full, occ * s->sms);
   if (const char* e = getenv("NS_ED_GRID")) s->grid_ed = std::max(1, std::min(occ * s->sms, atoi(e)));
   return NS_OK;
 }

@@ -113,11 +113,9 @@ __device__ void reflector_from_sigma(int n, int jj, const md::mdv<K>& sig, const
 }
 
 __device__ __forceinline__ void flag_wait(const int* f, int v) {
-  for (;;) {
-    int cur;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(cur) : "l"(f) : "memory");
-    if (cur >= v) break;
+  while (ld_relaxed_s32(f) < v) {
   }
+  fence_acq_rel();
 }
 // all lanes' prior writes are ordered by the caller's __syncwarp; the release
 // store (after an acq_rel fence, cumulative) publishes them

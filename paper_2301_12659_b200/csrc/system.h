@@ -28,7 +28,8 @@ struct ns_system {
   int* job_counter = nullptr;
   // eval/diff job queue (evaldiff.cuh): jobs, series pool, progress counters
   int4* jobs = nullptr;
-  int njobs = 0;
+  int njobs = 0, njobs_full = 0;
+  int eq_lo = 0, eq_hi = 0;  // equations evaluated by this handle (ns_set_partition)
   long long* ser_off = nullptr;
   double* pool = nullptr;
   int* prog = nullptr;       // [2M]: fprog, gprog
