@@ -80,7 +80,7 @@ struct GridBarrier {
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
       while ((int)(ld_relaxed_u32(cnt) - target) < 0) {
       }
-      fence_acq_rel();
+      (void)ld_acquire_u32(cnt);  // one acquire (one L1 invalidation) once the count is seen
     }
     __syncthreads();
   }

@@ -115,7 +115,7 @@ __device__ __forceinline__ void wait_geq(const int* p, int v) {
     __nanosleep(ns);
     ns = min(ns * 2, 512);
   }
-  fence_acq_rel();
+  (void)ld_acquire(p);
 }
 __device__ __forceinline__ void publish(int* p, int v) {
   __threadfence();
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
           __nanosleep(ns);
           ns = min(ns * 2, 512);
         }
-        fence_acq_rel();
+        (void)ld_acquire(J.left + tau);
       }
     for (int t = threadIdx.x; t < K * d; t += blockDim.x) {
       const int l = t / d, k = t % d;

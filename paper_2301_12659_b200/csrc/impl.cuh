@@ -88,7 +88,7 @@ ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
                   s->cmax, s->TB, k_lo};
   unsigned* bar = s->bar + 2;
   void* args[] = {&ds, &a, &bar};
-  CK(cudaLaunchCooperativeKernel((const void*)ns::stage_kernel<K>, dim3(s->grid_st), dim3(128), args, 0, st));
+  CK(cudaLaunchCooperativeKernel((const void*)ns::stage_kernel<K>, dim3(s->grid_st), dim3(s->st_threads), args, 0, st));
   s->last_launches += 1;
   return NS_OK;
 }
@@ -127,7 +127,9 @@ ns_status setup_grids(ns_system* s) {
       CK(cudaFuncSetAttribute(ns::householder_qr_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   }
   if (const char* e = getenv("NS_QR_GRID")) s->grid_qr = std::max(1, std::min(s->sms * occ, atoi(e)));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::stage_kernel<K>, 128, 0));
+  s->st_threads = 256;
+  if (const char* e = getenv("NS_STAGE_THREADS")) s->st_threads = atoi(e) >= 256 ? 256 : 128;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::stage_kernel<K>, s->st_threads, 0));
   if (occ < 1) return NS_ECUDA;
   s->grid_st = s->sms;
   {

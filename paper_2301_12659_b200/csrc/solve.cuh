@@ -115,12 +115,13 @@ __device__ void reflector_from_sigma(int n, int jj, const md::mdv<K>& sig, const
 __device__ __forceinline__ void flag_wait(const int* f, int v) {
   while (ld_relaxed_s32(f) < v) {
   }
-  fence_acq_rel();
+  int cur;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(cur) : "l"(f) : "memory");
+  (void)cur;
 }
 // all lanes' prior writes are ordered by the caller's __syncwarp; the release
 // store (after an acq_rel fence, cumulative) publishes them
 __device__ __forceinline__ void flag_set(int* f, int v) {
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
 }
 
@@ -381,7 +382,7 @@ struct StageArgs {
 constexpr int UCH = 64;  // update terms per chunk (32 lanes x 2)
 
 template <int K>
-__global__ void __launch_bounds__(128) stage_kernel(DevSys s, StageArgs a, unsigned* bar) {
+__global__ void __launch_bounds__(256) stage_kernel(DevSys s, StageArgs a, unsigned* bar) {
   GridBarrier gb(bar, 0u);
   const int n = s.n, d = s.d, nnz = s.nnz;
   const int gw = gwarp(), nw = nwarps(), lane = lane_id();

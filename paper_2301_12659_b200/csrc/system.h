@@ -38,7 +38,8 @@ struct ns_system {
   unsigned* bar = nullptr;     // [4]: qr barrier, stage barrier
   unsigned* status = nullptr;  // device status word
   int grid_ed = 0, grid_qr = 0, grid_st = 0;
-  size_t qr_smem_reserve = 0;  // dynamic smem requested by the QR kernel to own its SMs
+  size_t qr_smem_reserve = 0;
+  int st_threads = 256;        // threads per CTA of the stage kernel  // dynamic smem requested by the QR kernel to own its SMs
   size_t ed_smem = 0;
   bool qr_cached = false;
   cudaStream_t last_stream = nullptr;
