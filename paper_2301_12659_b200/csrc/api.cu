@@ -109,7 +109,7 @@ ns_status collect_ledger(ns_system* s) {
 void free_all(ns_system* s) {
   void* ptrs[] = {s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst, s->row_ptr, s->col_idx, s->job_order,
                   s->coeff, s->rhs, s->b, s->A, s->A0, s->W, s->vhead, s->beta, s->rdiag, s->R, s->Qt,
-                  s->invR, s->bp, s->dx, s->y, s->part, s->Minv, s->Z, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
+                  s->invR, s->bp, s->dx, s->y, s->part, s->Minv, s->Z, s->pend, s->sflags, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
                   s->bar, s->status, s->bws, s->A0q, s->qr_flags, s->jobs, s->ser_off, s->pool, s->prog, s->left,
                   s->left_init};
   for (void* p : ptrs)
@@ -294,6 +294,8 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->dx, (size_t)K * d * n) == cudaSuccess;
   ok &= dalloc(&s->y, (size_t)K * n) == cudaSuccess;
   ok &= dalloc(&s->Minv, (size_t)K * nn) == cudaSuccess;
+  ok &= dalloc(&s->pend, (size_t)K * d * n) == cudaSuccess;
+  ok &= dalloc(&s->sflags, 2 * d + 2) == cudaSuccess;
   ok &= dalloc(&s->Z, (size_t)K * nn) == cudaSuccess;
   {
     int maxlen = 1;

@@ -55,7 +55,7 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
             s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
   const double* xp = x;
   void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch};
-  CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_kernel<K>, dim3(s->grid_qr), dim3(128),
+  CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_kernel<K>, dim3(s->grid_qr), dim3(s->qr_threads),
                                  args, s->qr_smem_reserve, st));
   const long long tot = (long long)K * n * n;
   const int blocks = (int)std::min<long long>((tot + 255) / 256, 4LL * s->sms);
@@ -80,6 +80,23 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
 
 template <int K>
 ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
+  const int wpb = s->st_threads / 32;
+  const int Q = (s->n + wpb - 1) / wpb;
+  if (s->use_m && k_lo == 0 && s->stage_split && Q <= s->grid_st / 2 && s->d >= 3) {
+    // split design: critical group + right-looking bulk updates
+    CK(cudaMemsetAsync(s->bar + 2, 0, 2 * sizeof(unsigned), st));
+    CK(cudaMemsetAsync(s->sflags, 0, sizeof(int) * (2 * s->d + 2), st));
+    DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
+              s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
+    ns::Stage2Args a{s->b, s->A, s->Minv, s->bp, s->dx, s->pend, s->sflags, s->sflags + s->d,
+                     (unsigned*)(s->sflags + 2 * s->d), Q};
+    unsigned* bar = s->bar + 2;
+    void* args[] = {&ds, &a, &bar};
+    CK(cudaLaunchCooperativeKernel((const void*)ns::stage2_kernel<K>, dim3(s->grid_st), dim3(s->st_threads), args,
+                                   0, st));
+    s->last_launches += 1;
+    return NS_OK;
+  }
   CK(cudaMemsetAsync(s->bar + 2, 0, 2 * sizeof(unsigned), st));
   CK(cudaMemsetAsync(s->dx, 0, sizeof(double) * (size_t)K * s->d * s->n, st));
   DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
@@ -95,7 +112,13 @@ ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
 
 template <int K>
 ns_status launch_residual(ns_system* s, double* x, double* res_out, cudaStream_t st) {
-  ns::residual_kernel<K><<<s->d, 256, 0, st>>>(s->n, s->d, 0, s->b, s->bp, s->A0, s->dx, s->rbuf, s->knorm);
+  {
+    const long long rows = (long long)s->d * s->n;
+    const int blocks = (int)std::max<long long>(1, std::min<long long>((rows + 7) / 8, 8LL * s->sms));
+    ns::residual_kernel<K><<<blocks, 256, 0, st>>>(s->n, s->d, 0, s->b, s->bp, s->A0, s->dx, s->rbuf, s->knorm);
+    ns::knorm_kernel<K><<<s->d, 96, 0, st>>>(s->n, s->d, 0, s->b, s->rbuf, s->dx, s->knorm);
+    s->last_launches += 1;
+  }
   const long long tot = (long long)s->n * s->d;
   const int blocks = (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, 2LL * s->sms));
   ns::finalize_kernel<K><<<blocks, 256, 0, st>>>(s->n, s->d, x, s->dx, s->knorm,
@@ -112,7 +135,10 @@ ns_status setup_grids(ns_system* s) {
   if (occ < 1) return NS_ECUDA;
   // cooperative grids: enough warps for the 2n columns of [A0 | I], never more
   // CTAs than SMs (a grid barrier costs more with every CTA); env overrides for tuning
-  s->grid_qr = std::min(s->sms, std::max(1, (2 * s->n + 3) / 4));
+  // one warp per column of [A0 | I] while that fits in one CTA per SM of 4 warps;
+  // larger systems use 8 warps per CTA (the column updates are throughput work)
+  s->qr_threads = (2 * s->n > 4 * s->sms) ? 256 : 128;
+  s->grid_qr = std::min(s->sms, std::max(1, (2 * s->n + s->qr_threads / 32 - 1) / (s->qr_threads / 32)));
   // The QR is latency-bound and runs concurrently with eval/diff; a large
   // dynamic shared-memory request keeps eval/diff CTAs off the QR's SMs
   // (NS_QR_RESERVE=0 disables).  Default: reserve when the QR grid is small
@@ -129,6 +155,13 @@ ns_status setup_grids(ns_system* s) {
   if (const char* e = getenv("NS_QR_GRID")) s->grid_qr = std::max(1, std::min(s->sms * occ, atoi(e)));
   s->st_threads = 256;
   if (const char* e = getenv("NS_STAGE_THREADS")) s->st_threads = atoi(e) >= 256 ? 256 : 128;
+  s->stage_split = true;
+  if (const char* e = getenv("NS_STAGE_SPLIT")) s->stage_split = atoi(e) != 0;
+  {
+    int occ2 = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, ns::stage2_kernel<K>, s->st_threads, 0));
+    if (occ2 < 1) s->stage_split = false;
+  }
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::stage_kernel<K>, s->st_threads, 0));
   if (occ < 1) return NS_ECUDA;
   s->grid_st = s->sms;

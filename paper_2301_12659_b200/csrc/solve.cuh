@@ -133,7 +133,7 @@ __device__ __forceinline__ void flag_set(int* f, int v) {
 // (look-ahead of one column), so the critical path is one column update plus
 // one reflector per step.  n <= 128 rows per lane-register window (4 x 32).
 template <int K>
-__global__ void __launch_bounds__(128) householder_qr_kernel(DevSys sy, const double* __restrict__ x, int n,
+__global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const double* __restrict__ x, int n,
                                                              const double* __restrict__ A0,
                                                              double* W, double* vhead, double* beta,
                                                              double* rdiag, unsigned* bar,
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(128) householder_qr_kernel(DevSys sy, const do
     if (c0 >= ncol) break;  // nothing left for this warp
     if (j > 0) flag_wait(fA + j, epoch);  // column 0 was final at the start
     __syncwarp();
-    constexpr int MAXC = 4;  // columns per warp kept in flight (ncol <= 4 nw)
+    constexpr int MAXC = 4;  // partial dots kept in flight per warp (more columns: dot recomputed)
     md::mdv<K> part[MAXC];
     int nc = 0;
     for (int c = c0; c < ncol && nc < MAXC; c += nw, ++nc) {
@@ -500,19 +500,130 @@ __global__ void __launch_bounds__(256) stage_kernel(DevSys s, StageArgs a, unsig
   }
 }
 
+// ------------------------------------------------------------------ stage loop, split design
+// Right-looking updates off the critical path.  CTAs [0, Q) (the critical
+// group, one warp per row) run the dependent chain
+//   b'_k = pend_k - A_1 dx_{k-1};  sub-barrier;  dx_k = M b'_k;  sub-barrier;  publish dx_k
+// while CTAs [Q, G) (the bulk group) apply, as soon as dx_k is published,
+//   pend_{k'} -= A_{k'-k} dx_k   for every k' >= k + 2, every row,
+// each (k', row) pair owned by one bulk warp that takes k = 0, 1, ... in order,
+// so pend_{k'} = b_{k'} - sum_{j >= 2} A_j dx_{k'-j} accumulates in a fixed
+// order (deterministic).  pdone[k'] counts rows whose pend_{k'} is complete.
+struct Stage2Args {
+  const double* b;     // [K][d][n]
+  const double* A;     // [K][d][nnz]
+  const double* M;     // [K][n][n]
+  double* bp;          // [K][d][n]   b'_k
+  double* dx;          // [K][d][n]
+  double* pend;        // [K][d][n]   pending right-hand sides
+  int* dxr;            // [d] dx_k published (0/1, zeroed per launch)
+  int* pdone;          // [d] rows of pend_k complete
+  unsigned* cbar;      // critical-group barrier counter (zeroed per launch)
+  int Q;               // CTAs in the critical group
+};
+
+__device__ __forceinline__ void sub_sync(unsigned* cnt, unsigned& target, unsigned nq) {
+  __syncthreads();
+  target += nq;
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    while ((int)(ld_relaxed_u32(cnt) - target) < 0) {
+    }
+    (void)ld_acquire_u32(cnt);
+  }
+  __syncthreads();
+}
+
+template <int K>
+__device__ md::mdv<K> row_dot_A(const DevSys& s, const double* A, int j, const double* v, long long lsV, int i) {
+  // sum_e A_j[e] v[col e] over the structural entries of row i; warp-wide
+  const int lane = threadIdx.x & 31;
+  const long long lsA = (long long)s.d * s.nnz;
+  const int r0 = s.row_ptr[i], r1 = s.row_ptr[i + 1];
+  md::mdv<K> acc = md::zero<K>();
+  for (int e = r0 + lane; e < r1; e += 32)
+    acc = md::fma_acc<K>(acc, md::load<K>(A + (long long)j * s.nnz, lsA, e), md::load_cg<K>(v, lsV, s.col_idx[e]));
+  return md::group_sum<K>(acc, 32);
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, unsigned* bar) {
+  const int n = s.n, d = s.d;
+  const long long lsV = (long long)d * n, lsM = (long long)n * n;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  // prologue: pend = b (all CTAs), one full barrier
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)K * d * n;
+       t += (long long)gridDim.x * blockDim.x)
+    __stcg(a.pend + t, a.b[t]);
+  {
+    GridBarrier gb(bar, 0u);
+    gb.sync();
+  }
+  if ((int)blockIdx.x < a.Q) {
+    // ---------------- critical group
+    const int cw = blockIdx.x * wpb + wib, ncw = a.Q * wpb;
+    unsigned target = 0;
+    for (int k = 0; k < d; ++k) {
+      if (k >= 2) {
+        if (threadIdx.x == 0) flag_wait(a.pdone + k, n);
+        __syncthreads();
+      }
+      for (int i = cw; i < n; i += ncw) {
+        md::mdv<K> v = md::load_cg<K>(a.pend + (long long)k * n, lsV, i);
+        if (k >= 1) v = md::sub<K>(v, row_dot_A<K>(s, a.A, 1, a.dx + (long long)(k - 1) * n, lsV, i));
+        if (lane == 0) md::store_cg<K>(a.bp + (long long)k * n, lsV, i, v);
+      }
+      sub_sync(a.cbar, target, a.Q);
+      for (int r = cw; r < n; r += ncw) {
+        md::mdv<K> acc = md::zero<K>();
+        for (int c = lane; c < n; c += 32)
+          acc = md::fma_acc<K>(acc, md::load<K>(a.M, lsM, (long long)r * n + c),
+                               md::load_cg<K>(a.bp + (long long)k * n, lsV, c));
+        acc = md::group_sum<K>(acc, 32);
+        if (lane == 0) md::store_cg<K>(a.dx + (long long)k * n, lsV, r, acc);
+      }
+      sub_sync(a.cbar, target, a.Q);
+      if (blockIdx.x == 0 && threadIdx.x == 0) flag_set(a.dxr + k, 1);
+    }
+  } else {
+    // ---------------- bulk group: (k', i) pairs, k' = 2..d-1, dealt to bulk warps
+    const int bw = (blockIdx.x - a.Q) * wpb + wib, nbw = ((int)gridDim.x - a.Q) * wpb;
+    const int npairs = (d - 2) * n;
+    for (int k = 0; k + 2 < d; ++k) {
+      bool any = false;
+      for (int p = bw; p < npairs; p += nbw) any |= (2 + p / n >= k + 2);
+      if (!any) break;
+      if (lane == 0) flag_wait(a.dxr + k, 1);
+      __syncwarp();
+      for (int p = bw; p < npairs; p += nbw) {
+        const int kp = 2 + p / n, i = p % n;
+        if (kp < k + 2) continue;
+        const md::mdv<K> dot = row_dot_A<K>(s, a.A, kp - k, a.dx + (long long)k * n, lsV, i);
+        if (lane == 0) {
+          const long long e = (long long)kp * n;
+          md::store_cg<K>(a.pend + e, lsV, i, md::sub<K>(md::load_cg<K>(a.pend + e, lsV, i), dot));
+          if (k == kp - 2) {  // last contribution to pend_{k'} row i
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.pdone + kp) : "memory");
+          }
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ residual and norms
-// One CTA per coefficient k: r_k,i = b'_k,i - sum_c A0[i][c] dx_k[c];
-// knorm[k][0..2] = sum_i |b_k,i|, sum_i |r_k,i|, sum_i |dx_k,i|   (md, [3][K][d])
+// r_k,i = b'_k,i - sum_c A0[i][c] dx_k[c]: warps over all (k, i) rows of the grid.
 template <int K>
 __global__ void __launch_bounds__(256) residual_kernel(int n, int d, int k_lo, const double* __restrict__ b,
                                                        const double* __restrict__ bp,
                                                        const double* __restrict__ A0,
                                                        const double* __restrict__ dx, double* rbuf,
                                                        double* knorm) {
-  const int k = blockIdx.x;
-  const int w = threadIdx.x >> 5, nwb = blockDim.x >> 5, lane = lane_id();
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const long long lsV = (long long)d * n, lsM = (long long)n * n;
-  for (int i = w; i < n; i += nwb) {
+  for (long long row = gw; row < (long long)d * n; row += nw) {
+    const int k = (int)(row / n), i = (int)(row % n);
     md::mdv<K> acc = md::zero<K>();
     if (k >= k_lo) {
       for (int c = lane; c < n; c += 32) {
@@ -528,19 +639,24 @@ __global__ void __launch_bounds__(256) residual_kernel(int n, int d, int k_lo, c
       md::store<K>(rbuf + (long long)k * n, lsV, i, r);
     }
   }
-  __syncthreads();
-  // three 1-norms, one warp each, fixed order
-  if (w < 3) {
-    const double* src = (w == 0) ? b : ((w == 1) ? rbuf : dx);
-    md::mdv<K> acc = md::zero<K>();
-    for (int i = lane; i < n; i += 32) {
-      md::mdv<K> v = md::load<K>(src + (long long)k * n, lsV, i);
-      if (w == 2 && k < k_lo) v = md::zero<K>();
-      acc = md::add<K>(acc, md::absv<K>(v));
-    }
-    acc = md::group_sum<K>(acc, 32);
-    if (lane == 0) md::store<K>(knorm + (long long)w * K * d, d, k, acc);
+}
+
+// knorm[w][k] = sum_i |v_k,i| for v = b, r, dx (one CTA per k, one warp per norm)
+template <int K>
+__global__ void __launch_bounds__(96) knorm_kernel(int n, int d, int k_lo, const double* __restrict__ b,
+                                                   const double* __restrict__ rbuf, const double* __restrict__ dx,
+                                                   double* knorm) {
+  const int k = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long lsV = (long long)d * n;
+  const double* src = (w == 0) ? b : ((w == 1) ? rbuf : dx);
+  md::mdv<K> acc = md::zero<K>();
+  for (int i = lane; i < n; i += 32) {
+    md::mdv<K> v = md::load<K>(src + (long long)k * n, lsV, i);
+    if (w == 2 && k < k_lo) v = md::zero<K>();
+    acc = md::add<K>(acc, md::absv<K>(v));
   }
+  acc = md::group_sum<K>(acc, 32);
+  if (lane == 0) md::store<K>(knorm + (long long)w * K * d, d, k, acc);
 }
 
 // x += dx (one thread per coefficient); warp 0 of block 0 reduces the norms.

@@ -39,7 +39,11 @@ struct ns_system {
   unsigned* status = nullptr;  // device status word
   int grid_ed = 0, grid_qr = 0, grid_st = 0;
   size_t qr_smem_reserve = 0;
-  int st_threads = 256;        // threads per CTA of the stage kernel  // dynamic smem requested by the QR kernel to own its SMs
+  int st_threads = 256;        // threads per CTA of the stage kernel
+  int qr_threads = 128;        // threads per CTA of the QR kernel
+  bool stage_split = true;     // critical group + right-looking bulk updates (stage2_kernel)
+  double* pend = nullptr;      // [K][d][n] pending right-hand sides (stage2)
+  int* sflags = nullptr;       // [2d + 2] dx published, pend rows done, critical barrier  // dynamic smem requested by the QR kernel to own its SMs
   size_t ed_smem = 0;
   bool qr_cached = false;
   cudaStream_t last_stream = nullptr;
