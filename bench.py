@@ -153,10 +153,15 @@ def oracle_sample(sys_, x_np, budget_s: float, rotate: int = 0):
         acc += stage_cost[ks]
         ks += 1
     t0 = time.perf_counter()
+    if frac >= 0.999:
+        # the budget covers the whole step: run it (no extrapolation)
+        O.step(sys_, x_np, F, split=True)
+        dt = time.perf_counter() - t0
+        return dt, 1.0, f"oracle (mpmath {F.name}) full step (eval/diff of all {n} equations + block solve of all {d} stages)"
     xs = O.read_x(x_np, F)
     b_s, A_s = O.evaluate(sys_, xs, F, split=True, rows=rows)
     # the solve needs every row of A_0..A_{ks-1}: evaluate the solve's inputs on a
-    # truncated series (first ks coefficients) -- cheap relative to the full d
+    # truncated series (first ks coefficients)
     import copy
     sub = copy.copy(sys_)
     sub.D = ks - 1
@@ -167,7 +172,7 @@ def oracle_sample(sys_, x_np, budget_s: float, rotate: int = 0):
     dt = time.perf_counter() - t0
     tri_k = ks * (ks + 1) // 2
     done = sum(rows_cost[i] for i in rows) + sum(c // tri * tri_k for c in rows_cost) + n ** 3 // 3 + acc
-    frac_done = done / full
+    frac_done = min(1.0, done / full)
     desc = (f"oracle (mpmath {F.name}) on {len(rows)}/{n} equations for eval/diff plus the block solve "
             f"of stages 0..{ks - 1} (with their truncated eval/diff); {frac_done:.3f} of the step's "
             f"oracle multiply-adds, extrapolated by that count")
