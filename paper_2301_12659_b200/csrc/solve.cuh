@@ -91,8 +91,9 @@ __device__ void apply_reflector(int n, int j, int c, double* W, const double* vh
 }
 
 // Reflector jj from sigma = sum_{r >= jj} x_r^2 (already reduced over the
-// warp) and x0 = x_jj: alpha = -sign(x0) sqrt(sigma), v0 = x0 - alpha,
-// beta = -1/(alpha v0); writes vhead, beta, rdiag and W[jj][jj] = alpha.
+// warp) and x0 = x_jj: alpha = -sign(x0) sqrt(sigma), v0 = x0 - alpha; writes
+// vhead = v0, beta slot = alpha v0 (consumers form beta = -1/(alpha v0)), rdiag
+// and W[jj][jj] = alpha.
 template <int K>
 __device__ void reflector_from_sigma(int n, int jj, const md::mdv<K>& sig, const md::mdv<K>& x0, double* W,
                                      double* vhead, double* beta, double* rdiag, unsigned* status) {
@@ -101,12 +102,13 @@ __device__ void reflector_from_sigma(int n, int jj, const md::mdv<K>& sig, const
   const md::mdv<K> nrm = md::sqrt<K>(sig);
   const md::mdv<K> alpha = md::is_negative<K>(x0) ? nrm : md::neg<K>(nrm);
   const md::mdv<K> v0 = md::sub<K>(x0, alpha);
-  md::mdv<K> bt = md::zero<K>();
-  if (!md::is_zero<K>(sig)) bt = md::neg<K>(md::recip<K>(md::mul<K>(alpha, v0)));
+  // beta = -1/(alpha v0) is formed by the consumers; store alpha v0 (0 for a zero column)
+  md::mdv<K> pav = md::zero<K>();
+  if (!md::is_zero<K>(sig)) pav = md::mul<K>(alpha, v0);
   else if (lane == 0 && status) atomicOr(status, ST_SINGULAR);
   if (lane == 0) {
     md::store_cg<K>(vhead, n, jj, v0);
-    md::store_cg<K>(beta, n, jj, bt);
+    md::store_cg<K>(beta, n, jj, pav);
     md::store_cg<K>(rdiag, n, jj, alpha);
     md::store_cg<K>(W, ls, (long long)jj * n + jj, alpha);
   }
@@ -179,17 +181,38 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
   // after B[j] it adds v0 W[j][c] and applies the update.
   int* fA = flags;
   int* fB = flags + n;
+  constexpr int S = (K == 8) ? 2 : 4;  // rows per lane kept in registers (32 S rows)
   for (int j = 0; j < n; ++j) {
-    // first owned column > j
+    // first owned column > j (the look-ahead column j+1 is always its owner's first)
     int c0 = gw;
     if (c0 <= j) c0 += ((j - gw) / nw + 1) * nw;
     if (c0 >= ncol) break;  // nothing left for this warp
     if (j > 0) flag_wait(fA + j, epoch);  // column 0 was final at the start
     __syncwarp();
+    // v rows (r > j) and the first column's rows (r >= j) in registers: slot s holds
+    // row j + lane + 32 s; rows beyond 32 S are streamed from L2
+    md::mdv<K> vr[S], wr[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+      const int r = j + lane + 32 * q;
+      vr[q] = (r > j && r < n) ? md::load_cg<K>(W, ls, (long long)j * n + r) : md::zero<K>();
+      wr[q] = (r < n) ? md::load_cg<K>(W, ls, (long long)c0 * n + r) : md::zero<K>();
+    }
     constexpr int MAXC = 4;  // partial dots kept in flight per warp (more columns: dot recomputed)
     md::mdv<K> part[MAXC];
-    int nc = 0;
-    for (int c = c0; c < ncol && nc < MAXC; c += nw, ++nc) {
+    {
+      md::mdv<K> p = md::zero<K>();
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const int r = j + lane + 32 * q;
+        if (r > j && r < n) p = md::fma_acc<K>(p, vr[q], wr[q]);
+      }
+      for (int r = j + lane + 32 * S; r < n; r += 32)
+        p = md::fma_acc<K>(p, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)c0 * n + r));
+      part[0] = md::group_sum<K>(p, 32);
+    }
+    int nc = 1;
+    for (int c = c0 + nw; c < ncol && nc < MAXC; c += nw, ++nc) {
       md::mdv<K> p = md::zero<K>();
       for (int r = j + 1 + lane; r < n; r += 32)
         p = md::fma_acc<K>(p, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)c * n + r));
@@ -198,7 +221,10 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
     flag_wait(fB + j, epoch);
     __syncwarp();
     const md::mdv<K> v0 = md::load_cg<K>(vhead, n, j);
-    const md::mdv<K> bt = md::load_cg<K>(beta, n, j);
+    const md::mdv<K> pav = md::load_cg<K>(beta, n, j);  // alpha_j v0_j
+    // beta_j = -1 / (alpha v0), formed here (each consumer) so that the owner's
+    // critical chain ends at alpha v0; zero column -> beta = 0 (H = I)
+    const md::mdv<K> bt = md::is_zero<K>(pav) ? md::zero<K>() : md::neg<K>(md::recip<K>(pav));
     int ic = 0;
     for (int c = c0; c < ncol; c += nw, ++ic) {
       md::mdv<K> dot;
@@ -210,16 +236,36 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
           p = md::fma_acc<K>(p, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)c * n + r));
         dot = md::group_sum<K>(p, 32);
       }
-      dot = md::fma_acc<K>(dot, v0, md::load_cg<K>(W, ls, (long long)c * n + j));
+      const bool first = (ic == 0);
+      const md::mdv<K> wj = first ? md::shfl<K>(wr[0], 0) : md::load_cg<K>(W, ls, (long long)c * n + j);
+      dot = md::fma_acc<K>(dot, v0, wj);
       const md::mdv<K> nw_ = md::neg<K>(md::mul<K>(bt, dot));
       const bool look = (c == j + 1 && c < n);
       md::mdv<K> sig = md::zero<K>(), x0 = md::zero<K>();
-      for (int r = j + lane; r < n; r += 32) {
-        const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
-        const md::mdv<K> w = md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)c * n + r), nw_, v);
-        md::store_cg<K>(W, ls, (long long)c * n + r, w);
-        if (look && r > j) sig = md::fma_acc<K>(sig, w, w);  // look-ahead norm, same pass
-        if (r == j + 1) x0 = w;
+      if (first) {
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+          const int r = j + lane + 32 * q;
+          if (r < n) {
+            const md::mdv<K> v = (r == j) ? v0 : vr[q];
+            const md::mdv<K> w = md::fma_acc<K>(wr[q], nw_, v);
+            md::store_cg<K>(W, ls, (long long)c * n + r, w);
+            if (look && r > j) sig = md::fma_acc<K>(sig, w, w);  // look-ahead norm, same pass
+            if (r == j + 1) x0 = w;
+          }
+        }
+        for (int r = j + lane + 32 * S; r < n; r += 32) {
+          const md::mdv<K> w =
+              md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)c * n + r), nw_, md::load_cg<K>(W, ls, (long long)j * n + r));
+          md::store_cg<K>(W, ls, (long long)c * n + r, w);
+          if (look) sig = md::fma_acc<K>(sig, w, w);
+        }
+      } else {
+        for (int r = j + lane; r < n; r += 32) {
+          const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
+          const md::mdv<K> w = md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)c * n + r), nw_, v);
+          md::store_cg<K>(W, ls, (long long)c * n + r, w);
+        }
       }
       if (look) {
         __syncwarp();
