@@ -343,6 +343,37 @@ MD_INL bool greater(const mdv<K>& a, const mdv<K>& b) {
   return d.x[0] > 0.0;
 }
 
+// ---------------------------------------------------------------- multi-accumulator dot
+// sum_{t in [t0, t1) step dt} x(t) * y(t) with NA independent accumulators
+// (round robin, combined in a fixed order at the end): NA times the ILP of a
+// single accumulation chain.  Deterministic for fixed (t0, t1, dt).
+template <int K, int NA, typename F>
+MD_INL mdv<K> dot_ilp(int t0, int t1, int dt, F term) {
+  mdv<K> acc[NA];
+#pragma unroll
+  for (int a = 0; a < NA; ++a) acc[a] = zero<K>();
+  int t = t0;
+  for (; t + (NA - 1) * dt < t1; t += NA * dt) {
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      mdv<K> x, y;
+      term(t + a * dt, x, y);
+      acc[a] = fma_acc<K>(acc[a], x, y);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NA; ++a) {
+    if (t + a * dt < t1) {
+      mdv<K> x, y;
+      term(t + a * dt, x, y);
+      acc[a] = fma_acc<K>(acc[a], x, y);
+    }
+  }
+#pragma unroll
+  for (int a = 1; a < NA; ++a) acc[0] = add<K>(acc[0], acc[a]);
+  return acc[0];
+}
+
 // ---------------------------------------------------------------- warp shuffles
 template <int K>
 MD_INL mdv<K> shfl_xor(const mdv<K>& a, int mask, int width = 32) {

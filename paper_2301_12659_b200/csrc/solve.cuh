@@ -213,9 +213,10 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
     }
     int nc = 1;
     for (int c = c0 + nw; c < ncol && nc < MAXC; c += nw, ++nc) {
-      md::mdv<K> p = md::zero<K>();
-      for (int r = j + 1 + lane; r < n; r += 32)
-        p = md::fma_acc<K>(p, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)c * n + r));
+      const md::mdv<K> p = md::dot_ilp<K, 2>(j + 1 + lane, n, 32, [&](int r, md::mdv<K>& xa, md::mdv<K>& yb) {
+        xa = md::load_cg<K>(W, ls, (long long)j * n + r);
+        yb = md::load_cg<K>(W, ls, (long long)c * n + r);
+      });
       part[nc] = md::group_sum<K>(p, 32);
     }
     flag_wait(fB + j, epoch);
@@ -384,23 +385,21 @@ __global__ void __launch_bounds__(128) form_m_kernel(int n, int TB, const double
     for (int w = gw; w < (t1 - t0) * jg; w += nw) {
       const int r = t0 + w / jg, j = (w % jg) * 32 + lane;
       if (j < n) {
-        md::mdv<K> acc = md::load<K>(Qt, lsM, (long long)r * n + j);
-#pragma unroll 4
-        for (int c = t1; c < n; ++c)
-          acc = md::fma_acc<K>(acc, md::neg<K>(md::load<K>(R, lsM, (long long)r * n + c)),
-                               md::load_cg<K>(M, lsM, (long long)c * n + j));
-        md::store_cg<K>(Z, lsM, (long long)r * n + j, acc);
+        const md::mdv<K> acc = md::dot_ilp<K, 4>(t1, n, 1, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
+          xa = md::load<K>(R, lsM, (long long)r * n + c);
+          yb = md::load_cg<K>(M, lsM, (long long)c * n + j);
+        });
+        md::store_cg<K>(Z, lsM, (long long)r * n + j, md::sub<K>(md::load<K>(Qt, lsM, (long long)r * n + j), acc));
       }
     }
     gb.sync();
     for (int w = gw; w < (t1 - t0) * jg; w += nw) {
       const int r = t0 + w / jg, j = (w % jg) * 32 + lane;
       if (j < n) {
-        md::mdv<K> acc = md::zero<K>();
-#pragma unroll 4
-        for (int c = t0; c < t1; ++c)
-          acc = md::fma_acc<K>(acc, md::load<K>(invR, lsI, (long long)t * TB * TB + (long long)(r - t0) * TB + (c - t0)),
-                               md::load_cg<K>(Z, lsM, (long long)c * n + j));
+        const md::mdv<K> acc = md::dot_ilp<K, 4>(t0, t1, 1, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
+          xa = md::load<K>(invR, lsI, (long long)t * TB * TB + (long long)(r - t0) * TB + (c - t0));
+          yb = md::load_cg<K>(Z, lsM, (long long)c * n + j);
+        });
         md::store_cg<K>(M, lsM, (long long)r * n + j, acc);
       }
     }
@@ -586,9 +585,10 @@ __device__ md::mdv<K> row_dot_A(const DevSys& s, const double* A, int j, const d
   const int lane = threadIdx.x & 31;
   const long long lsA = (long long)s.d * s.nnz;
   const int r0 = s.row_ptr[i], r1 = s.row_ptr[i + 1];
-  md::mdv<K> acc = md::zero<K>();
-  for (int e = r0 + lane; e < r1; e += 32)
-    acc = md::fma_acc<K>(acc, md::load<K>(A + (long long)j * s.nnz, lsA, e), md::load_cg<K>(v, lsV, s.col_idx[e]));
+  const md::mdv<K> acc = md::dot_ilp<K, 2>(r0 + lane, r1, 32, [&](int e, md::mdv<K>& xa, md::mdv<K>& yb) {
+    xa = md::load<K>(A + (long long)j * s.nnz, lsA, e);
+    yb = md::load_cg<K>(v, lsV, s.col_idx[e]);
+  });
   return md::group_sum<K>(acc, 32);
 }
 
@@ -621,10 +621,10 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
       }
       sub_sync(a.cbar, target, a.Q);
       for (int r = cw; r < n; r += ncw) {
-        md::mdv<K> acc = md::zero<K>();
-        for (int c = lane; c < n; c += 32)
-          acc = md::fma_acc<K>(acc, md::load<K>(a.M, lsM, (long long)r * n + c),
-                               md::load_cg<K>(a.bp + (long long)k * n, lsV, c));
+        md::mdv<K> acc = md::dot_ilp<K, 2>(lane, n, 32, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
+          xa = md::load<K>(a.M, lsM, (long long)r * n + c);
+          yb = md::load_cg<K>(a.bp + (long long)k * n, lsV, c);
+        });
         acc = md::group_sum<K>(acc, 32);
         if (lane == 0) md::store_cg<K>(a.dx + (long long)k * n, lsV, r, acc);
       }
