@@ -370,10 +370,9 @@ ns_status ns_newton_series_step(ns_system* s, int precision, int dim, int degree
   if (dim != s->n || degree != s->D) return NS_EDIM;
   if (flags & ~(NS_REUSE_QR | NS_NO_RESIDUAL | NS_LEDGER | NS_TILED_BS)) return NS_EINVAL;
   if ((flags & NS_REUSE_QR) && !s->qr_cached) return NS_ESTATE;
-  // M = R^{-1} Q^T costs ~n^3/2 md-FMA once per QR and saves 2T barriers per
-  // stage: worth it for n <= 256; larger systems use the per-stage tiled path.
+  // M = R^{-1} Q^T (~n^3/2 md-FMA once per QR) saves 2T barriers per stage.
   // With NS_REUSE_QR the cached factorisation keeps the form it was made in.
-  if (!(flags & NS_REUSE_QR)) s->use_m = !(flags & NS_TILED_BS) && s->n <= 256;
+  if (!(flags & NS_REUSE_QR)) s->use_m = !(flags & NS_TILED_BS);
   cudaStream_t st = (cudaStream_t)stream;
   switch (s->K) {
     case 2: return step_impl<2>(s, x, res_out, flags, st);
@@ -449,7 +448,7 @@ ns_status ns_newton_series_step_from(ns_system* s, int precision, int dim, int d
   CK(cudaMemcpyAsync(s->b, b, sizeof(double) * K * d * n, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(s->A, A, sizeof(double) * K * d * s->nnz, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(s->A0, A0, sizeof(double) * K * n * n, cudaMemcpyDeviceToDevice, st));
-  if (!(flags & NS_REUSE_QR)) s->use_m = !(flags & NS_TILED_BS) && s->n <= 256;
+  if (!(flags & NS_REUSE_QR)) s->use_m = !(flags & NS_TILED_BS);
   ns_status r = NS_OK;
   switch (s->K) {
     case 2:
@@ -489,7 +488,7 @@ ns_status ns_toeplitz_solve(ns_system* s, const double* b, const double* A, cons
   CK(cudaMemcpyAsync(s->A0q, A0, sizeof(double) * K * n * n, cudaMemcpyDeviceToDevice, st));
   ns_status r;
   s->last_launches = 0;
-  s->use_m = s->n <= 256;
+  s->use_m = true;
   switch (s->K) {
     case 2: r = Impl<2>::qr(s, s->A0q, nullptr, st); if (!r) r = Impl<2>::stage(s, 0, st); break;
     case 4: r = Impl<4>::qr(s, s->A0q, nullptr, st); if (!r) r = Impl<4>::stage(s, 0, st); break;

@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
     }
     int nc = 1;
     for (int c = c0 + nw; c < ncol && nc < MAXC; c += nw, ++nc) {
-      const md::mdv<K> p = md::dot_ilp<K, 2>(j + 1 + lane, n, 32, [&](int r, md::mdv<K>& xa, md::mdv<K>& yb) {
+      const md::mdv<K> p = md::dot_ilp<K, 1>(j + 1 + lane, n, 32, [&](int r, md::mdv<K>& xa, md::mdv<K>& yb) {
         xa = md::load_cg<K>(W, ls, (long long)j * n + r);
         yb = md::load_cg<K>(W, ls, (long long)c * n + r);
       });
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(128) form_m_kernel(int n, int TB, const double
     for (int w = gw; w < (t1 - t0) * jg; w += nw) {
       const int r = t0 + w / jg, j = (w % jg) * 32 + lane;
       if (j < n) {
-        const md::mdv<K> acc = md::dot_ilp<K, 4>(t1, n, 1, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
+        const md::mdv<K> acc = md::dot_ilp<K, (K == 8 ? 4 : 1)>(t1, n, 1, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
           xa = md::load<K>(R, lsM, (long long)r * n + c);
           yb = md::load_cg<K>(M, lsM, (long long)c * n + j);
         });
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(128) form_m_kernel(int n, int TB, const double
     for (int w = gw; w < (t1 - t0) * jg; w += nw) {
       const int r = t0 + w / jg, j = (w % jg) * 32 + lane;
       if (j < n) {
-        const md::mdv<K> acc = md::dot_ilp<K, 4>(t0, t1, 1, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
+        const md::mdv<K> acc = md::dot_ilp<K, (K == 8 ? 4 : 1)>(t0, t1, 1, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
           xa = md::load<K>(invR, lsI, (long long)t * TB * TB + (long long)(r - t0) * TB + (c - t0));
           yb = md::load_cg<K>(Z, lsM, (long long)c * n + j);
         });
@@ -585,7 +585,7 @@ __device__ md::mdv<K> row_dot_A(const DevSys& s, const double* A, int j, const d
   const int lane = threadIdx.x & 31;
   const long long lsA = (long long)s.d * s.nnz;
   const int r0 = s.row_ptr[i], r1 = s.row_ptr[i + 1];
-  const md::mdv<K> acc = md::dot_ilp<K, 2>(r0 + lane, r1, 32, [&](int e, md::mdv<K>& xa, md::mdv<K>& yb) {
+  const md::mdv<K> acc = md::dot_ilp<K, 1>(r0 + lane, r1, 32, [&](int e, md::mdv<K>& xa, md::mdv<K>& yb) {
     xa = md::load<K>(A + (long long)j * s.nnz, lsA, e);
     yb = md::load_cg<K>(v, lsV, s.col_idx[e]);
   });
@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
       }
       sub_sync(a.cbar, target, a.Q);
       for (int r = cw; r < n; r += ncw) {
-        md::mdv<K> acc = md::dot_ilp<K, 2>(lane, n, 32, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
+        md::mdv<K> acc = md::dot_ilp<K, 1>(lane, n, 32, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
           xa = md::load<K>(a.M, lsM, (long long)r * n + c);
           yb = md::load_cg<K>(a.bp + (long long)k * n, lsV, c);
         });
