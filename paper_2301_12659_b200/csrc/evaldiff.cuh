@@ -117,8 +117,18 @@ __device__ __forceinline__ void wait_geq(const int* p, int v) {
   }
   (void)ld_acquire(p);
 }
+// asynchronous global -> shared copy of one double (cp.async, no register staging)
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+}
+
+// the CTA's pool writes are ordered before this by __syncthreads; the release
+// store is cumulative (no separate fence)
 __device__ __forceinline__ void publish(int* p, int v) {
-  __threadfence();
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
@@ -156,16 +166,30 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
         const int len = fwd ? m - 1 : m - 2;
         double* base = fwd ? F : G;
         double* sbuf[2] = {bacc + K * d, bacc + 2 * K * d};
+        double* xbuf[2] = {bacc + 3 * K * d, bacc + 4 * K * d};  // prefetched x series
+        auto vidx = [&](int q) { return fwd ? vars[q] : vars[m - 1 - q]; };
+        // x_{v(1)} (the first b operand) into xbuf[1]
+        for (int t = threadIdx.x; t < K * d; t += blockDim.x) {
+          const int l = t / d, k = t % d;
+          cp_async8(&xbuf[1][l * d + k], x + (long long)l * xs + (long long)vidx(1) * d + k);
+        }
+        cp_async_wait_all();
+        __syncthreads();
         for (int q = 1; q <= len; ++q) {
           double* outp = base + (q - 1) * ser;
+          // prefetch the next step's operand x_{v(q+1)} while this convolution runs
+          if (q + 1 <= len)
+            for (int t = threadIdx.x; t < K * d; t += blockDim.x) {
+              const int l = t / d, k = t % d;
+              cp_async8(&xbuf[(q + 1) & 1][l * d + k], x + (long long)l * xs + (long long)vidx(q + 1) * d + k);
+            }
           auto get = [&](int, SerRef& pa, SerRef& pb, double*& pc) {
-            const int v0 = fwd ? vars[0] : vars[m - 1];
-            const int vq = fwd ? vars[q] : vars[m - 1 - q];
-            pa = (q == 1) ? SerRef{x + (long long)v0 * d, xs} : SerRef{sbuf[(q - 1) & 1], d};
-            pb = SerRef{x + (long long)vq * d, xs};
+            pa = (q == 1) ? SerRef{x + (long long)vidx(0) * d, xs} : SerRef{sbuf[(q - 1) & 1], d};
+            pb = SerRef{xbuf[q & 1], d};
             pc = sbuf[q & 1];
           };
           conv_batch<K>(threadIdx.x, blockDim.x, 1, d, get, &outp);
+          cp_async_wait_all();  // the next operand has landed (copy overlapped the convolution)
           __syncthreads();
           if (threadIdx.x == 0) publish(fwd ? J.fprog + tau : J.gprog + tau, q);
         }

@@ -170,7 +170,7 @@ ns_status setup_grids(ns_system* s) {
     CK(cudaFuncSetAttribute(ns::invert_tiles_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)inv_smem));
   }
   if (const char* e = getenv("NS_STAGE_GRID")) s->grid_st = std::max(1, std::min(s->sms * occ, atoi(e)));
-  s->ed_smem = 3 * sizeof(double) * (size_t)K * s->d;  // b accumulator + chain double buffer
+  s->ed_smem = 5 * sizeof(double) * (size_t)K * s->d;  // b accumulator, chain + x double buffers
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::evaldiff_jobs_kernel<K>, 256, s->ed_smem));
   if (occ < 1) return NS_ECUDA;
   s->grid_ed = std::min(s->njobs_full, occ * s->sms);
