@@ -159,6 +159,11 @@ ns_status ns_md_latency_probe(int precision, int op, double* cycles_per_op);
 
 /* Synchronises the handle's last stream and returns the device status word. */
 ns_status ns_get_status(ns_system* sys, ns_step_info* host_out);
+/* Job trace of the last eval/diff (handle created with env NS_TRACE=1): per job
+ * [pop, inputs ready, done] globaltimer nanoseconds into host[3*i..], the job
+ * descriptors {type, monomial/equation, j, key} into jobs_out[4*i..] (may be
+ * NULL).  Synchronises.  Returns the number of jobs, -1 without a trace. */
+int32_t ns_get_trace(ns_system* sys, int64_t* host, int32_t capacity_jobs, int32_t* jobs_out);
 /* Synchronises; per-class milliseconds accumulated over steps run with NS_LEDGER. */
 ns_status ns_get_ledger(ns_system* sys, ns_ledger* host_out);
 ns_status ns_reset_ledger(ns_system* sys);

@@ -33,7 +33,7 @@ EXPORTS = ["ns_system_create", "ns_system_destroy", "ns_newton_series_step",
            "ns_toeplitz_solve", "ns_get_r_diag", "ns_md_op", "ns_get_status", "ns_get_ledger",
            "ns_reset_ledger", "ns_last_launch_count", "ns_strerror", "ns_build_info",
            "ns_fp64_peak_probe", "ns_md_latency_probe", "ns_barrier_probe", "ns_set_partition",
-           "ns_newton_series_step_from"]
+           "ns_newton_series_step_from", "ns_get_trace"]
 
 
 class NSError(RuntimeError):
@@ -83,6 +83,7 @@ def lib() -> ctypes.CDLL:
                                            u32, vp], ctypes.c_int),
         "ns_eval_diff": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
         "ns_set_partition": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+        "ns_get_trace": ([vp, vp, i32, vp], i32),
         "ns_newton_series_step_from": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, u32, vp],
                                        ctypes.c_int),
         "ns_nnz": ([vp], i32),
@@ -262,6 +263,16 @@ class NewtonSystem:
 
     def reset_ledger(self):
         _check(lib().ns_reset_ledger(self._h), "ns_reset_ledger")
+
+    def trace(self):
+        """Job trace of the last eval/diff (env NS_TRACE=1 at create): (times [J][3] ns, jobs [J][4])."""
+        cap = 1 << 22
+        t = np.zeros((cap, 3), np.int64)
+        jb = np.zeros((cap, 4), np.int32)
+        nj = int(lib().ns_get_trace(self._h, t.ctypes.data, cap, jb.ctypes.data))
+        if nj < 0:
+            raise RuntimeError("no trace (create the handle with NS_TRACE=1)")
+        return t[:nj], jb[:nj]
 
     def last_launch_count(self) -> int:
         return int(lib().ns_last_launch_count(self._h))

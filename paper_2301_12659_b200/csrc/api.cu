@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <set>
@@ -111,7 +112,7 @@ void free_all(ns_system* s) {
                   s->coeff, s->rhs, s->b, s->A, s->A0, s->W, s->vhead, s->beta, s->rdiag, s->R, s->Qt,
                   s->invR, s->bp, s->dx, s->y, s->part, s->Minv, s->Z, s->pend, s->sflags, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
                   s->bar, s->status, s->bws, s->A0q, s->qr_flags, s->jobs, s->ser_off, s->pool, s->prog, s->left,
-                  s->left_init};
+                  s->left_init, s->trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& row : s->ev)
@@ -323,6 +324,8 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->prog, 2 * (size_t)M) == cudaSuccess;
   ok &= dalloc(&s->left, M) == cudaSuccess;
   ok &= dalloc(&s->left_init, M) == cudaSuccess;
+  if (const char* e = getenv("NS_TRACE"))
+    if (atoi(e)) ok &= dalloc(&s->trace, 3 * jobs.size()) == cudaSuccess;
   if (!ok) return fail(NS_ENOMEM);
   ok &= cudaMemcpy(s->jobs, jobs.data(), sizeof(int4) * jobs.size(), cudaMemcpyHostToDevice) == cudaSuccess;
   ok &= cudaMemcpy(s->ser_off, ser_off.data(), sizeof(long long) * M, cudaMemcpyHostToDevice) == cudaSuccess;
@@ -417,6 +420,26 @@ ns_status ns_eval_diff(ns_system* s, const double* x, double* b, double* A, doub
 }
 
 int32_t ns_nnz(const ns_system* s) { return s ? s->nnz : -1; }
+
+int32_t ns_get_trace(ns_system* s, int64_t* host, int32_t capacity_jobs, int32_t* jobs_out) {
+  if (!s || !s->trace) return -1;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  const int nj = std::min(capacity_jobs, s->njobs);
+  if (host && nj > 0) {
+    if (cudaMemcpy(host, s->trace, sizeof(long long) * 3 * nj, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  }
+  if (jobs_out) {
+    std::vector<int4> jb(nj);
+    if (cudaMemcpy(jb.data(), s->jobs, sizeof(int4) * nj, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    for (int i = 0; i < nj; ++i) {
+      jobs_out[4 * i] = jb[i].x;
+      jobs_out[4 * i + 1] = jb[i].y;
+      jobs_out[4 * i + 2] = jb[i].z;
+      jobs_out[4 * i + 3] = jb[i].w;
+    }
+  }
+  return nj;
+}
 
 ns_status ns_set_partition(ns_system* s, int eq_lo, int eq_hi) {
   if (!s || eq_lo < 0 || eq_hi > s->n || eq_lo >= eq_hi) return NS_EINVAL;

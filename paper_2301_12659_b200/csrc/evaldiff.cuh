@@ -102,7 +102,14 @@ struct EdJobs {
   int* fprog;                // [M] forward products done
   int* gprog;                // [M] backward products done
   int* left;                 // [M] chain + cross jobs not yet finished
+  long long* trace;          // [njobs][3] pop / inputs-ready / done globaltimer (ns), or nullptr
 };
+
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -142,9 +149,12 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
   __shared__ int4 s_job;
   extern __shared__ double bacc[];  // [K][d]
   for (;;) {
+    __shared__ int s_id;
     if (threadIdx.x == 0) {
       const int id = atomicAdd(job_counter, 1);
       s_job = (id < J.njobs) ? J.jobs[id] : make_int4(-1, 0, 0, 0);
+      s_id = id;
+      if (J.trace && id < J.njobs) J.trace[3LL * id] = gtimer();
     }
     __syncthreads();
     const int4 jb = s_job;
@@ -198,6 +208,7 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
         if (threadIdx.x == 0) {
           if (j - 2 >= 1) wait_geq(J.fprog + tau, j - 2);
           if (m - j - 1 >= 1) wait_geq(J.gprog + tau, m - j - 1);
+          if (J.trace) J.trace[3LL * s_id + 1] = gtimer();
         }
         __syncthreads();
         auto get = [&](int, SerRef& pa, SerRef& pb, double*& pc) {
@@ -212,6 +223,7 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
       if (threadIdx.x == 0) {
         __threadfence();
         atomicSub(J.left + tau, 1);
+        if (J.trace) J.trace[3LL * s_id + 2] = gtimer();
       }
       continue;
     }
@@ -227,6 +239,7 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
         }
         (void)ld_acquire(J.left + tau);
       }
+    if (threadIdx.x == 0 && J.trace) J.trace[3LL * s_id + 1] = gtimer();
     for (int t = threadIdx.x; t < K * d; t += blockDim.x) {
       const int l = t / d, k = t % d;
       bacc[l * d + k] = s.rhs[(long long)l * xs + (long long)i * d + k];
@@ -282,6 +295,7 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
       A0[((long long)l * n + i) * n + s.col_idx[e]] = A[(long long)l * d * nnz + e];
     }
     __syncthreads();
+    if (threadIdx.x == 0 && J.trace) J.trace[3LL * s_id + 2] = gtimer();
   }
 }
 

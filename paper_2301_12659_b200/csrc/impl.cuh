@@ -21,7 +21,7 @@ ns_status launch_evaldiff(ns_system* s, const double* x, cudaStream_t st) {
   CK(cudaMemcpyAsync(s->left, s->left_init, sizeof(int) * s->M, cudaMemcpyDeviceToDevice, st));
   DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
             s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
-  ns::EdJobs J{s->jobs, s->njobs, s->ser_off, s->pool, s->prog, s->prog + s->M, s->left};
+  ns::EdJobs J{s->jobs, s->njobs, s->ser_off, s->pool, s->prog, s->prog + s->M, s->left, s->trace};
   ns::evaldiff_jobs_kernel<K><<<s->grid_ed, 256, s->ed_smem, st>>>(ds, J, x, s->b, s->A, s->A0, s->job_counter);
   s->last_launches += 1;
   CK(cudaGetLastError());

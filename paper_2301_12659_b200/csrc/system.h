@@ -35,6 +35,7 @@ struct ns_system {
   int* prog = nullptr;       // [2M]: fprog, gprog
   int* left = nullptr;       // [M]
   int* left_init = nullptr;  // [M]
+  long long* trace = nullptr;  // [njobs][3] job trace (NS_TRACE=1 at create), else nullptr
   unsigned* bar = nullptr;     // [4]: qr barrier, stage barrier
   unsigned* status = nullptr;  // device status word
   int grid_ed = 0, grid_qr = 0, grid_st = 0;

@@ -1,0 +1,37 @@
+"""Trace the eval/diff job queue of one step (NS_TRACE=1) and summarise it."""
+import json
+import os
+import sys
+
+os.environ["NS_TRACE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2301_12659_b200 as P
+import synth
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+s = synth.build_config(cfg)
+h = P.NewtonSystem.from_system(s)
+x0 = torch.tensor(synth.make_x(s, "near", seed=1), device="cuda")
+for _ in range(3):
+    x = x0.clone()
+    h.step(x)
+torch.cuda.synchronize()
+t, jb = h.trace()
+t0 = t[:, 0].min()
+t = (t - t0) / 1e3  # us
+out = {"config": cfg, "njobs": int(len(t)), "span_us": float(t[:, 2].max())}
+for ty, name in ((0, "fwd_chain"), (1, "bwd_chain"), (2, "cross"), (3, "equation")):
+    sel = jb[:, 0] == ty
+    if sel.any():
+        dur = t[sel, 2] - np.where(t[sel, 1] > 0, t[sel, 1], t[sel, 0])
+        out[name] = {"count": int(sel.sum()), "first_pop": float(t[sel, 0].min()), "last_done": float(t[sel, 2].max()),
+                     "mean_run_us": float(dur.mean()), "max_run_us": float(dur.max())}
+# the longest chain: per-step time
+sel = (jb[:, 0] == 0)
+i = np.argmax(jb[:, 2] * sel)
+out["longest_fwd_chain"] = {"len": int(jb[i, 2]), "start": float(t[i, 0]), "done": float(t[i, 2]),
+                            "us_per_step": float((t[i, 2] - t[i, 0]) / max(1, jb[i, 2]))}
+print(json.dumps(out, indent=1))
