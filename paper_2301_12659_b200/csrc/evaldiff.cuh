@@ -36,8 +36,11 @@ template <int K, typename Get>
 __device__ void conv_batch(int tid, int T, int B, int d, Get get, double* const* c2 = nullptr) {
   const int P = (d + 1) / 2;
   const int groups = B * P;
+  // G lanes per coefficient pair; each lane should sum >= 4 of the d+1 terms
+  // (below that the md butterfly costs more than the multiply-adds; measured
+  // with the job trace: C2 chain steps 6 us with 2 terms per lane)
   int G = 1;
-  while (G < 32 && groups * G * 2 <= T) G <<= 1;
+  while (G < 32 && groups * G * 2 <= T && (d + 1) / (2 * G) >= 4) G <<= 1;
   const int per_round = T / G;
   const int sub = tid % G;
   for (int g0 = 0; g0 < groups; g0 += per_round) {
