@@ -40,7 +40,7 @@ __device__ void conv_batch(int tid, int T, int B, int d, Get get, double* const*
   // (below that the md butterfly costs more than the multiply-adds; measured
   // with the job trace: C2 chain steps 6 us with 2 terms per lane)
   int G = 1;
-  while (G < 32 && groups * G * 2 <= T && (d + 1) / (2 * G) >= 4) G <<= 1;
+  while (G < 32 && groups * G * 2 <= T && (d + 1) / (2 * G) >= 4) G <<= 1;  // >= 4 terms per lane
   const int per_round = T / G;
   const int sub = tid % G;
   for (int g0 = 0; g0 < groups; g0 += per_round) {
@@ -204,7 +204,9 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
           conv_batch<K>(threadIdx.x, blockDim.x, 1, d, get, &outp);
           cp_async_wait_all();  // the next operand has landed (copy overlapped the convolution)
           __syncthreads();
-          if (threadIdx.x == 0) publish(fwd ? J.fprog + tau : J.gprog + tau, q);
+          // the release store (a memory barrier) is issued by the last thread so that
+          // warp 0, which computes, does not stall on it
+          if (threadIdx.x == blockDim.x - 1) publish(fwd ? J.fprog + tau : J.gprog + tau, q);
         }
       } else {
         const int j = jb.z;  // 2..m-1
