@@ -325,7 +325,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->left, M) == cudaSuccess;
   ok &= dalloc(&s->left_init, M) == cudaSuccess;
   if (const char* e = getenv("NS_TRACE"))
-    if (atoi(e)) ok &= dalloc(&s->trace, 3 * jobs.size()) == cudaSuccess;
+    if (atoi(e)) ok &= dalloc(&s->trace, 3 * jobs.size() + 4 * 256) == cudaSuccess;
   if (!ok) return fail(NS_ENOMEM);
   ok &= cudaMemcpy(s->jobs, jobs.data(), sizeof(int4) * jobs.size(), cudaMemcpyHostToDevice) == cudaSuccess;
   ok &= cudaMemcpy(s->ser_off, ser_off.data(), sizeof(long long) * M, cudaMemcpyHostToDevice) == cudaSuccess;
@@ -427,6 +427,10 @@ int32_t ns_get_trace(ns_system* s, int64_t* host, int32_t capacity_jobs, int32_t
   const int nj = std::min(capacity_jobs, s->njobs);
   if (host && nj > 0) {
     if (cudaMemcpy(host, s->trace, sizeof(long long) * 3 * nj, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    if (capacity_jobs >= s->njobs + 342)  // step stamps of job 0 after the job records
+      if (cudaMemcpy(host + 3 * nj, s->trace + 3 * s->njobs, sizeof(long long) * 4 * 256, cudaMemcpyDeviceToHost) !=
+          cudaSuccess)
+        return -1;
   }
   if (jobs_out) {
     std::vector<int4> jb(nj);

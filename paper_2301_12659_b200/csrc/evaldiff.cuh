@@ -188,7 +188,9 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
         }
         cp_async_wait_all();
         __syncthreads();
+        long long* st_tr = (J.trace && s_id == 0) ? J.trace + 3LL * J.njobs : nullptr;  // step stamps of job 0
         for (int q = 1; q <= len; ++q) {
+          if (st_tr && threadIdx.x == 0 && q <= 256) st_tr[4 * (q - 1)] = clock64();
           double* outp = base + (q - 1) * ser;
           // prefetch the next step's operand x_{v(q+1)} while this convolution runs
           if (q + 1 <= len)
@@ -202,8 +204,10 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
             pc = sbuf[q & 1];
           };
           conv_batch<K>(threadIdx.x, blockDim.x, 1, d, get, &outp);
+          if (st_tr && threadIdx.x == 0 && q <= 256) st_tr[4 * (q - 1) + 1] = clock64();
           cp_async_wait_all();  // the next operand has landed (copy overlapped the convolution)
           __syncthreads();
+          if (st_tr && threadIdx.x == 0 && q <= 256) st_tr[4 * (q - 1) + 2] = clock64();
           // the release store (a memory barrier) is issued by the last thread so that
           // warp 0, which computes, does not stall on it
           if (threadIdx.x == blockDim.x - 1) publish(fwd ? J.fprog + tau : J.gprog + tau, q);
