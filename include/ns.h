@@ -164,6 +164,12 @@ ns_status ns_get_status(ns_system* sys, ns_step_info* host_out);
  * descriptors {type, monomial/equation, j, key} into jobs_out[4*i..] (may be
  * NULL).  Synchronises.  Returns the number of jobs, -1 without a trace. */
 int32_t ns_get_trace(ns_system* sys, int64_t* host, int32_t capacity_jobs, int32_t* jobs_out);
+/* Look-ahead trace of the last cluster QR (handle created with env
+ * NS_CQR_TRACE=1): per step j, 8 globaltimer stamps (ns) of the warp owning
+ * column j+1: [start, reflector rows in, partial dots done, v0 in, beta in,
+ * column updated, rows published, reflector j+1 published] into host[8*j..].
+ * Synchronises.  Returns the number of steps, -1 without a trace. */
+int32_t ns_get_qr_trace(ns_system* sys, int64_t* host, int32_t capacity_steps);
 /* Synchronises; per-class milliseconds accumulated over steps run with NS_LEDGER. */
 ns_status ns_get_ledger(ns_system* sys, ns_ledger* host_out);
 ns_status ns_reset_ledger(ns_system* sys);

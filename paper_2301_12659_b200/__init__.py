@@ -33,7 +33,7 @@ EXPORTS = ["ns_system_create", "ns_system_destroy", "ns_newton_series_step",
            "ns_toeplitz_solve", "ns_get_r_diag", "ns_md_op", "ns_get_status", "ns_get_ledger",
            "ns_reset_ledger", "ns_last_launch_count", "ns_strerror", "ns_build_info",
            "ns_fp64_peak_probe", "ns_md_latency_probe", "ns_barrier_probe", "ns_set_partition",
-           "ns_newton_series_step_from", "ns_get_trace"]
+           "ns_newton_series_step_from", "ns_get_trace", "ns_get_qr_trace"]
 
 
 class NSError(RuntimeError):
@@ -84,6 +84,7 @@ def lib() -> ctypes.CDLL:
         "ns_eval_diff": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
         "ns_set_partition": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "ns_get_trace": ([vp, vp, i32, vp], i32),
+        "ns_get_qr_trace": ([vp, vp, i32], i32),
         "ns_newton_series_step_from": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, u32, vp],
                                        ctypes.c_int),
         "ns_nnz": ([vp], i32),

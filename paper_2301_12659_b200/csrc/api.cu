@@ -325,7 +325,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->left, M) == cudaSuccess;
   ok &= dalloc(&s->left_init, M) == cudaSuccess;
   if (const char* e = getenv("NS_TRACE"))
-    if (atoi(e)) ok &= dalloc(&s->trace, 3 * jobs.size() + 4 * 256) == cudaSuccess;
+    if (atoi(e)) ok &= dalloc(&s->trace, 3 * jobs.size() + 6 * 256) == cudaSuccess;
   if (!ok) return fail(NS_ENOMEM);
   ok &= cudaMemcpy(s->jobs, jobs.data(), sizeof(int4) * jobs.size(), cudaMemcpyHostToDevice) == cudaSuccess;
   ok &= cudaMemcpy(s->ser_off, ser_off.data(), sizeof(long long) * M, cudaMemcpyHostToDevice) == cudaSuccess;
@@ -363,6 +363,7 @@ void ns_system_destroy(ns_system* s) {
   cudaSetDevice(s->dev);
   cudaDeviceSynchronize();
   free_all(s);
+  if (s->cqr_trace) cudaFree(s->cqr_trace);
   delete s;
 }
 
@@ -421,14 +422,24 @@ ns_status ns_eval_diff(ns_system* s, const double* x, double* b, double* A, doub
 
 int32_t ns_nnz(const ns_system* s) { return s ? s->nnz : -1; }
 
+int32_t ns_get_qr_trace(ns_system* s, int64_t* host, int32_t capacity_steps) {
+  if (!s || !s->cqr_trace) return -1;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  const int ns_ = std::min(capacity_steps, s->n);
+  if (host && ns_ > 0 &&
+      cudaMemcpy(host, s->cqr_trace, sizeof(long long) * 8 * ns_, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return ns_;
+}
+
 int32_t ns_get_trace(ns_system* s, int64_t* host, int32_t capacity_jobs, int32_t* jobs_out) {
   if (!s || !s->trace) return -1;
   if (cudaDeviceSynchronize() != cudaSuccess) return -1;
   const int nj = std::min(capacity_jobs, s->njobs);
   if (host && nj > 0) {
     if (cudaMemcpy(host, s->trace, sizeof(long long) * 3 * nj, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
-    if (capacity_jobs >= s->njobs + 342)  // step stamps of job 0 after the job records
-      if (cudaMemcpy(host + 3 * nj, s->trace + 3 * s->njobs, sizeof(long long) * 4 * 256, cudaMemcpyDeviceToHost) !=
+    if (capacity_jobs >= s->njobs + 512)  // step stamps of job 0 after the job records
+      if (cudaMemcpy(host + 3 * nj, s->trace + 3 * s->njobs, sizeof(long long) * 6 * 256, cudaMemcpyDeviceToHost) !=
           cudaSuccess)
         return -1;
   }

@@ -32,15 +32,21 @@ struct SerRef {
 // tid = 0..T-1 (a whole CTA, or one warp with T = 32).  get(bi, a, b, c)
 // returns the operands of convolution bi; outputs are compact series (limb
 // stride d).  T must be a multiple of 32 or equal to 32.
+// Conv tuning (EdJobs.conv_mode): bit 0 selects the per-term renormalising
+// accumulate (fma_acc, the first implementation); the default keeps each
+// lane's partial sums as unnormalised level arrays (md::dot_levels_insert: the
+// product's levels enter with exact two_sums, no renormalisation per term),
+// reduces them with the lazy butterfly and renormalises once.  min_terms:
+// the group width G doubles while every lane keeps >= min_terms terms.
 template <int K, typename Get>
-__device__ void conv_batch(int tid, int T, int B, int d, Get get, double* const* c2 = nullptr) {
+__device__ void conv_batch(int tid, int T, int B, int d, Get get, double* const* c2 = nullptr, int min_terms = 4,
+                           int mode = 0, long long* dbg = nullptr) {
   const int P = (d + 1) / 2;
   const int groups = B * P;
-  // G lanes per coefficient pair; each lane should sum >= 4 of the d+1 terms
-  // (below that the md butterfly costs more than the multiply-adds; measured
-  // with the job trace: C2 chain steps 6 us with 2 terms per lane)
+  // G lanes per coefficient pair; each lane sums >= min_terms of the d+1 terms
+  // (below that the md butterfly costs more than the multiply-adds)
   int G = 1;
-  while (G < 32 && groups * G * 2 <= T && (d + 1) / (2 * G) >= 4) G <<= 1;  // >= 4 terms per lane
+  while (G < 32 && groups * G * 2 <= T && (d + 1) / (2 * G) >= min_terms) G <<= 1;
   const int per_round = T / G;
   const int sub = tid % G;
   for (int g0 = 0; g0 < groups; g0 += per_round) {
@@ -50,29 +56,81 @@ __device__ void conv_batch(int tid, int T, int B, int d, Get get, double* const*
     const int p = active ? gid % P : 0;
     const int k1 = p, k2 = d - 1 - p;
     const int tot = active ? ((k1 == k2) ? k1 + 1 : d + 1) : 0;
-    md::mdv<K> acc1 = md::zero<K>(), acc2 = md::zero<K>();
     SerRef a, b;
     double* c;
     get(bi, a, b, c);
-    for (int t = sub; t < tot; t += G) {
-      const bool first = t <= k1;
-      const int k = first ? k1 : k2;
-      const int j = first ? t : t - k1 - 1;
-      md::mdv<K> xa = a.cg ? md::load_cg<K>(a.p, a.ls, j) : md::load<K>(a.p, a.ls, j);
-      md::mdv<K> yb = b.cg ? md::load_cg<K>(b.p, b.ls, k - j) : md::load<K>(b.p, b.ls, k - j);
-      md::mdv<K> cur;
+    md::mdv<K> acc1, acc2;
+    if (mode & 1) {
+      acc1 = md::zero<K>();
+      acc2 = md::zero<K>();
+      for (int t = sub; t < tot; t += G) {
+        const bool first = t <= k1;
+        const int k = first ? k1 : k2;
+        const int j = first ? t : t - k1 - 1;
+        md::mdv<K> xa = a.cg ? md::load_cg<K>(a.p, a.ls, j) : md::load<K>(a.p, a.ls, j);
+        md::mdv<K> yb = b.cg ? md::load_cg<K>(b.p, b.ls, k - j) : md::load<K>(b.p, b.ls, k - j);
+        md::mdv<K> cur;
 #pragma unroll
-      for (int l = 0; l < K; ++l) cur.x[l] = first ? acc1.x[l] : acc2.x[l];
-      cur = md::fma_acc<K>(cur, xa, yb);
+        for (int l = 0; l < K; ++l) cur.x[l] = first ? acc1.x[l] : acc2.x[l];
+        cur = md::fma_acc<K>(cur, xa, yb);
 #pragma unroll
-      for (int l = 0; l < K; ++l) {
-        acc1.x[l] = first ? cur.x[l] : acc1.x[l];
-        acc2.x[l] = first ? acc2.x[l] : cur.x[l];
+        for (int l = 0; l < K; ++l) {
+          acc1.x[l] = first ? cur.x[l] : acc1.x[l];
+          acc2.x[l] = first ? acc2.x[l] : cur.x[l];
+        }
       }
-    }
-    if (G > 1) {
-      acc1 = md::group_sum<K>(acc1, G);
-      acc2 = md::group_sum<K>(acc2, G);
+      if (G > 1) {
+        acc1 = md::group_sum<K>(acc1, G);
+        acc2 = md::group_sum<K>(acc2, G);
+      }
+    } else {
+      // unnormalised level sums, UC terms per unrolled chunk (loads and
+      // products of a chunk are independent; only the level inserts chain)
+      constexpr int UC = (K <= 4) ? 4 : 2;
+      double s1[K], s2[K];
+#pragma unroll
+      for (int l = 0; l < K; ++l) s1[l] = s2[l] = 0.0;
+      // one term into the level sums of its output (first: k1, else k2)
+      auto insert = [&](const md::mdv<K>& xa, const md::mdv<K>& yb, bool first) {
+        double pl[K];
+        md::prod_levels<K>(xa, yb, pl);
+        double sc[K];
+#pragma unroll
+        for (int l = 0; l < K; ++l) sc[l] = first ? s1[l] : s2[l];
+#pragma unroll
+        for (int l = 0; l < K; ++l) md::level_insert<K>(sc, l, pl[l]);
+#pragma unroll
+        for (int l = 0; l < K; ++l) {
+          s1[l] = first ? sc[l] : s1[l];
+          s2[l] = first ? s2[l] : sc[l];
+        }
+      };
+      auto operands = [&](int t, md::mdv<K>& xa, md::mdv<K>& yb, bool& first) {
+        first = t <= k1;
+        const int k = first ? k1 : k2;
+        const int j = first ? t : t - k1 - 1;
+        xa = a.cg ? md::load_cg<K>(a.p, a.ls, j) : md::load<K>(a.p, a.ls, j);
+        yb = b.cg ? md::load_cg<K>(b.p, b.ls, k - j) : md::load<K>(b.p, b.ls, k - j);
+      };
+      int t0 = sub;
+      for (; t0 + (UC - 1) * G < tot; t0 += UC * G) {  // full chunks
+        md::mdv<K> xa[UC], yb[UC];
+        bool fst[UC];
+#pragma unroll
+        for (int u = 0; u < UC; ++u) operands(t0 + u * G, xa[u], yb[u], fst[u]);
+#pragma unroll
+        for (int u = 0; u < UC; ++u) insert(xa[u], yb[u], fst[u]);
+      }
+      for (; t0 < tot; t0 += G) {  // tail terms
+        md::mdv<K> xa, yb;
+        bool first;
+        operands(t0, xa, yb, first);
+        insert(xa, yb, first);
+      }
+      if (dbg && tid == 0) dbg[0] = clock64();
+      acc1 = md::group_sum_levels<K>(s1, G);
+      acc2 = md::group_sum_levels<K>(s2, G);
+      if (dbg && tid == 0) dbg[1] = clock64();
     }
     if (active && sub == 0) {
       md::store<K>(c, d, k1, acc1);
@@ -106,6 +164,9 @@ struct EdJobs {
   int* gprog;                // [M] backward products done
   int* left;                 // [M] chain + cross jobs not yet finished
   long long* trace;          // [njobs][3] pop / inputs-ready / done globaltimer (ns), or nullptr
+  int conv_terms;            // conv_batch min_terms
+  int conv_mode;             // conv_batch mode bits (bit 0: per-term renormalising accumulate;
+                             // bit 1: cross jobs read their operands from the pool, no smem staging)
 };
 
 __device__ __forceinline__ long long gtimer() {
@@ -203,7 +264,8 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
             pb = SerRef{xbuf[q & 1], d};
             pc = sbuf[q & 1];
           };
-          conv_batch<K>(threadIdx.x, blockDim.x, 1, d, get, &outp);
+          conv_batch<K>(threadIdx.x, blockDim.x, 1, d, get, &outp, J.conv_terms, J.conv_mode,
+                        (st_tr && q <= 256) ? st_tr + 4 * 256 + 2 * (q - 1) : nullptr);
           if (st_tr && threadIdx.x == 0 && q <= 256) st_tr[4 * (q - 1) + 1] = clock64();
           cp_async_wait_all();  // the next operand has landed (copy overlapped the convolution)
           __syncthreads();
@@ -220,13 +282,30 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
           if (J.trace) J.trace[3LL * s_id + 1] = gtimer();
         }
         __syncthreads();
+        const int gq = m - j - 1;
+        SerRef ra = (j - 2 == 0) ? SerRef{x + (long long)vars[0] * d, xs} : SerRef{F + (j - 3) * ser, d, true};
+        SerRef rb = (gq == 0) ? SerRef{x + (long long)vars[m - 1] * d, xs} : SerRef{G + (gq - 1) * ser, d, true};
+        if (!(J.conv_mode & 2)) {
+          // both operands into shared memory (one L2 round trip instead of one per term chunk)
+          double* sa = bacc + K * d;
+          double* sb = bacc + 2 * K * d;
+          for (int t = threadIdx.x; t < 2 * K * d; t += blockDim.x) {
+            const int w = t / (K * d), r = t % (K * d);
+            const int l = r / d, k = r % d;
+            const SerRef& src = w ? rb : ra;
+            cp_async8((w ? sb : sa) + l * d + k, src.p + l * src.ls + k);
+          }
+          cp_async_wait_all();
+          __syncthreads();
+          ra = SerRef{sa, d};
+          rb = SerRef{sb, d};
+        }
         auto get = [&](int, SerRef& pa, SerRef& pb, double*& pc) {
-          pa = (j - 2 == 0) ? SerRef{x + (long long)vars[0] * d, xs} : SerRef{F + (j - 3) * ser, d, true};
-          const int gq = m - j - 1;
-          pb = (gq == 0) ? SerRef{x + (long long)vars[m - 1] * d, xs} : SerRef{G + (gq - 1) * ser, d, true};
+          pa = ra;
+          pb = rb;
           pc = X + (j - 2) * ser;
         };
-        conv_batch<K>(threadIdx.x, blockDim.x, 1, d, get);
+        conv_batch<K>(threadIdx.x, blockDim.x, 1, d, get, nullptr, J.conv_terms, J.conv_mode);
         __syncthreads();
       }
       if (threadIdx.x == 0) {

@@ -4,6 +4,7 @@
 #include <cstdlib>
 
 #include "batched.cuh"
+#include "cqr.cuh"
 #include "evaldiff.cuh"
 #include "md.cuh"
 #include "solve.cuh"
@@ -21,7 +22,8 @@ ns_status launch_evaldiff(ns_system* s, const double* x, cudaStream_t st) {
   CK(cudaMemcpyAsync(s->left, s->left_init, sizeof(int) * s->M, cudaMemcpyDeviceToDevice, st));
   DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
             s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
-  ns::EdJobs J{s->jobs, s->njobs, s->ser_off, s->pool, s->prog, s->prog + s->M, s->left, s->trace};
+  ns::EdJobs J{s->jobs, s->njobs, s->ser_off, s->pool, s->prog, s->prog + s->M, s->left, s->trace,
+                 s->conv_terms, s->conv_mode};
   ns::evaldiff_jobs_kernel<K><<<s->grid_ed, 256, s->ed_smem, st>>>(ds, J, x, s->b, s->A, s->A0, s->job_counter);
   s->last_launches += 1;
   CK(cudaGetLastError());
@@ -54,16 +56,44 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
   DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
             s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
   const double* xp = x;
-  void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch};
-  CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_kernel<K>, dim3(s->grid_qr), dim3(s->qr_threads),
-                                 args, s->qr_smem_reserve, st));
-  const long long tot = (long long)K * n * n;
-  const int blocks = (int)std::min<long long>((tot + 255) / 256, 4LL * s->sms);
-  ns::qr_unpack_kernel<K><<<blocks, 256, 0, st>>>(n, s->W, s->R, s->Qt);
-  const size_t inv_smem = sizeof(double) * (size_t)K * (2 * s->TB * s->TB + s->TB * s->TB / 2);
-  ns::invert_tiles_kernel<K><<<s->T, 256, inv_smem, st>>>(n, s->TB, s->R, s->invR);
-  s->last_launches += 3;
-  if (s->use_m) {
+  if (s->cqr_on) {
+    ns::CqrShape sh{s->cqr_P, s->cqr_W, s->cqr_CPC, s->cqr_RS, (s->cqr_withM && s->use_m) ? 1 : 0};
+    double* Mo = sh.withM ? s->Minv : nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(s->cqr_P);
+    cfg.blockDim = dim3(32 * s->cqr_W);
+    cfg.dynamicSmemBytes = s->cqr_smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = s->cqr_P;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    double *R = s->R, *Qt = s->Qt;
+    long long* tr = s->cqr_trace;
+    if (s->cqr_E == 2)
+      CK(cudaLaunchKernelEx(&cfg, ns::cluster_qr_kernel<K, 2>, ds, xp, n, A0, W, R, Qt, rd, stt, sh, tr, Mo));
+    else
+      CK(cudaLaunchKernelEx(&cfg, ns::cluster_qr_kernel<K, 4>, ds, xp, n, A0, W, R, Qt, rd, stt, sh, tr, Mo));
+    s->last_launches += 1;
+  } else {
+    void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch};
+    CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_kernel<K>, dim3(s->grid_qr), dim3(s->qr_threads),
+                                   args, s->qr_smem_reserve, st));
+    const long long tot = (long long)K * n * n;
+    const int blocks = (int)std::min<long long>((tot + 255) / 256, 4LL * s->sms);
+    ns::qr_unpack_kernel<K><<<blocks, 256, 0, st>>>(n, s->W, s->R, s->Qt);
+    s->last_launches += 2;
+  }
+  const bool m_done = s->cqr_on && s->cqr_withM && s->use_m;  // M formed inside the cluster QR
+  if (!m_done) {
+    const size_t inv_smem = sizeof(double) * (size_t)K * (2 * s->TB * s->TB + s->TB * s->TB / 2);
+    ns::invert_tiles_kernel<K><<<s->T, 256, inv_smem, st>>>(n, s->TB, s->R, s->invR);
+    s->last_launches += 1;
+  }
+  if (s->use_m && !m_done) {
     CK(cudaMemsetAsync(s->bar + 4, 0, 2 * sizeof(unsigned), st));
     int TB = s->TB;
     const double *R = s->R, *Qt = s->Qt, *iR = s->invR;
@@ -152,10 +182,80 @@ ns_status setup_grids(ns_system* s) {
     if (reserve)
       CK(cudaFuncSetAttribute(ns::householder_qr_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
   }
+  // cluster QR: the whole [A0 | I] in the shared memory of one cluster of P CTAs
+  {
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->dev));
+    s->cqr_on = false;
+    // octo double: the trailing updates outweigh the chain on 16 SMs (C3 measured
+    // slower than the grid-wide QR), so the cluster QR is for K <= 4
+    bool want = s->n <= 128 && K <= 4;
+    if (const char* e = getenv("NS_CQR")) want = want && atoi(e) != 0;
+    int Pforce = 0, RS = 8;
+    if (const char* e = getenv("NS_CQR_P")) Pforce = atoi(e);
+    if (const char* e = getenv("NS_CQR_RS")) RS = std::max(2, atoi(e));
+    const int wmax = (K == 8) ? 8 : 16;
+    for (int P : {16, 8}) {
+      if (!want || s->cqr_on || (Pforce && P != Pforce)) continue;
+      const int CPC = (2 * s->n + P - 1) / P;
+      const int W = std::min(wmax, CPC);
+      if (2 * W < CPC) continue;
+      ns::CqrShape sh{P, W, CPC, RS, 1};
+      size_t smem = ns::cqr_smem_bytes(s->n, K, sh);
+      bool withM = smem <= (size_t)optin;
+      if (const char* e = getenv("NS_CQR_M")) withM = withM && atoi(e) != 0;
+      if (!withM) {
+        sh.withM = 0;
+        smem = ns::cqr_smem_bytes(s->n, K, sh);
+      }
+      if (smem > (size_t)optin) continue;
+      // the QR chain is latency-bound: keep eval/diff CTAs off the cluster's SMs
+      // with the full shared-memory request (NS_CQR_RESERVE=0: only what it needs)
+      bool reserve = true;
+      if (const char* e = getenv("NS_CQR_RESERVE")) reserve = atoi(e) != 0;
+      if (reserve) smem = (size_t)optin;
+      auto kern = (s->n <= 64) ? ns::cluster_qr_kernel<K, 2> : ns::cluster_qr_kernel<K, 4>;
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) continue;
+      if (P > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(P);
+      cfg.blockDim = dim3(32 * W);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = P;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl < 1) {
+        cudaGetLastError();
+        continue;
+      }
+      s->cqr_on = true;
+      s->cqr_P = P;
+      s->cqr_W = W;
+      s->cqr_CPC = CPC;
+      s->cqr_RS = RS;
+      s->cqr_E = (s->n <= 64) ? 2 : 4;
+      s->cqr_smem = smem;
+      s->cqr_withM = withM;
+      if (getenv("NS_CQR_TRACE") && !s->cqr_trace) {
+        if (cudaMalloc(&s->cqr_trace, sizeof(long long) * 8 * s->n) != cudaSuccess) s->cqr_trace = nullptr;
+        else cudaMemset(s->cqr_trace, 0, sizeof(long long) * 8 * s->n);
+      }
+    }
+  }
   if (const char* e = getenv("NS_QR_GRID")) s->grid_qr = std::max(1, std::min(s->sms * occ, atoi(e)));
   s->st_threads = 256;
   if (const char* e = getenv("NS_STAGE_THREADS")) s->st_threads = atoi(e) >= 256 ? 256 : 128;
   s->stage_split = true;
+  if (const char* e = getenv("NS_CONV_TERMS")) s->conv_terms = std::max(1, atoi(e));
+  if (const char* e = getenv("NS_CONV_MODE")) s->conv_mode = atoi(e);
   if (const char* e = getenv("NS_STAGE_SPLIT")) s->stage_split = atoi(e) != 0;
   {
     int occ2 = 0;

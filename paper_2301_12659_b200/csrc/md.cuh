@@ -442,6 +442,36 @@ MD_INL mdv<K> group_sum(mdv<K> v, int G) {
   }
 }
 
+// group_sum of unnormalised level arrays (lane partial sums kept as levels):
+// the same butterfly, one renormalisation at the end (also for G == 1).
+template <int K>
+MD_INL mdv<K> group_sum_levels(const double (&s0)[K], int G) {
+  const int lane = threadIdx.x & 31;
+  double s[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) s[i] = s0[i];
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    if (off < G) {
+      double o[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) o[i] = __shfl_xor_sync(0xffffffffu, s[i], off);
+      const bool hi = (lane & off) != 0;
+      double lo_s[K], hi_s[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        lo_s[i] = hi ? o[i] : s[i];
+        hi_s[i] = hi ? s[i] : o[i];
+      }
+#pragma unroll
+      for (int i = 0; i < K; ++i) s[i] = lo_s[i];
+#pragma unroll
+      for (int l = 0; l < K; ++l) level_insert<K>(s, l, hi_s[l]);
+    }
+  }
+  return renorm<K, K>(s);
+}
+
 // ---------------------------------------------------------------- memory (limb planes)
 // value i of a planar md array: limb l at base[l * stride + i]
 template <int K>

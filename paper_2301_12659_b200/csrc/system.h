@@ -42,6 +42,13 @@ struct ns_system {
   size_t qr_smem_reserve = 0;
   int st_threads = 256;        // threads per CTA of the stage kernel
   int qr_threads = 128;        // threads per CTA of the QR kernel
+  bool cqr_on = false;         // cluster QR (cqr.cuh) instead of householder_qr_kernel
+  int cqr_P = 0, cqr_W = 0, cqr_CPC = 0, cqr_RS = 0, cqr_E = 0;
+  size_t cqr_smem = 0;
+  bool cqr_withM = false;          // M = R^-1 Q^T formed inside the cluster QR
+  long long* cqr_trace = nullptr;  // NS_CQR_TRACE: [n][8] look-ahead stamps (ns_get_qr_trace)
+  int conv_terms = 4;          // eval/diff conv: min terms per lane (NS_CONV_TERMS)
+  int conv_mode = 0;           // eval/diff conv mode bits (NS_CONV_MODE, evaldiff.cuh)
   bool stage_split = true;     // critical group + right-looking bulk updates (stage2_kernel)
   double* pend = nullptr;      // [K][d][n] pending right-hand sides (stage2)
   int* sflags = nullptr;       // [2d + 2] dx published, pend rows done, critical barrier  // dynamic smem requested by the QR kernel to own its SMs

@@ -33,6 +33,7 @@ raw = np.zeros((cap, 3), np.int64)
 jbr = np.zeros((cap, 4), np.int32)
 nj = P.lib().ns_get_trace(h._h, raw.ctypes.data, cap, jbr.ctypes.data)
 steps = raw.reshape(-1)[3 * nj: 3 * nj + 4 * 256].reshape(256, 4)
+inner = raw.reshape(-1)[3 * nj + 4 * 256: 3 * nj + 6 * 256].reshape(256, 2)
 L = int(jbr[0, 2]) if jbr[0, 0] <= 1 else 0
 if L:
     st = steps[:L]
@@ -40,7 +41,10 @@ if L:
     sync = (st[:, 2] - st[:, 1]).astype(float)
     gap = (st[1:, 0] - st[:-1, 2]).astype(float)
     step_stats = {"job0_len": L, "conv_cycles_mean": float(conv.mean()), "conv_cycles_min": float(conv.min()),
-                  "wait_sync_cycles_mean": float(sync.mean()), "gap_cycles_mean": float(gap.mean()) if L > 1 else 0.0}
+                  "wait_sync_cycles_mean": float(sync.mean()),
+                  "terms_cycles_mean": float((inner[:L, 0] - st[:, 0]).mean()),
+                  "butterfly_cycles_mean": float((inner[:L, 1] - inner[:L, 0]).mean()),
+                  "store_cycles_mean": float((st[:, 1] - inner[:L, 1]).mean()), "gap_cycles_mean": float(gap.mean()) if L > 1 else 0.0}
 else:
     step_stats = {}
 t0 = t[:, 0].min()
