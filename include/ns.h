@@ -64,6 +64,11 @@ typedef enum {
                              P:124-126); default: dx_k = M b'_k with M = R^{-1} Q^T formed
                              once per factorisation (same algebra, one matvec per stage)  */
 
+#define NS_QR_ONCE 16u    /* ns_run_newton: factor A_0 in the first iteration only, the
+                             paper's "the QR decomposition happens only once";
+                             default: refactor while stage 0 is active (reading R34)      */
+#define NS_NO_STAGGER 32u /* ns_run_newton: all orders 0..D in every iteration           */
+
 typedef struct ns_system ns_system; /* opaque; owns all device workspace */
 
 typedef struct {
@@ -83,6 +88,25 @@ typedef struct {
   uint32_t status_bits;  /* 1 = zero R_jj seen, 2 = non-finite norm                   */
   int32_t qr_cached;     /* 1 if a factorisation is cached for NS_REUSE_QR            */
 } ns_step_info;
+
+/* One iteration of ns_run_newton (staggered Newton).  Norms are the
+ * leading limbs of the md norms (max over the active k of the vector 1-norm). */
+typedef struct {
+  int32_t iter;        /* 1-based                                               */
+  int32_t k_lo, dc;    /* active stage window [k_lo, dc) of this iteration      */
+  int32_t qr;          /* 1 if A_0 was factored in this iteration               */
+  double norm_b;       /* ||b||  over k < dc                            */
+  double norm_r;       /* ||b - A dx|| over k < dc                      */
+  double norm_dx;      /* ||dx||                                        */
+  double ms;           /* device time of the iteration's step (CUDA events)     */
+} ns_iter_log;
+
+typedef struct {
+  int32_t iterations;  /* iterations run (<= max_iter)                          */
+  int32_t converged;   /* 1: every stage 0..D retired (reading R34)             */
+  int32_t qr_count;    /* factorisations of A_0 performed                       */
+  int32_t k_lo;        /* stages retired at exit                                */
+} ns_run_info;
 
 /* kernel classes of T4; updates, qhb and bs are fused into one
  * persistent stage kernel and reported together as "stage" */
@@ -159,6 +183,39 @@ ns_status ns_md_latency_probe(int precision, int op, double* cycles_per_op);
 
 /* Synchronises the handle's last stream and returns the device status word. */
 ns_status ns_get_status(ns_system* sys, ns_step_info* host_out);
+
+/* Active stage window of the following steps (staggered computations,
+ * P:494-518): a step evaluates and differentiates at coefficients 0..dc-1
+ * only (the products of Eq.(14) truncated at t^dc), solves the stages
+ * k = k_lo..dc-1 with dx_k = 0 for the retired stages k < k_lo (Eq.(11):
+ * b_k = 0 => dx_k = 0), updates x_k for k < dc only (x_k, k >= dc, are left
+ * unchanged) and takes the norms over k < dc.  0 <= k_lo < dc <= degree + 1,
+ * else NS_EINVAL.  ns_set_window(sys, 0, degree + 1) restores the full step.
+ * Host-side state; stream-ordered with the steps that follow. */
+ns_status ns_set_window(ns_system* sys, int k_lo, int dc);
+
+/* Per-stage norms of the last step (synchronises its stream): host_out
+ * [4][K][D+1] md values sum_i |v_k,i| for v = b, b - A dx, dx and x (x before
+ * the update); entries k >= dc of the last window are stale. */
+ns_status ns_get_stage_norms(ns_system* sys, double* host_out);
+
+/* The staggered Newton driver (P:304-325 with P:494-518, SPEC run_newton):
+ * x (device [K][dim][D+1], in/out) is the start series, x_0 accurate to about
+ * half the working precision.  Iteration i runs one step on the
+ * window [k_lo, dc): dc starts at 1 and grows by d := d + 1 + floor(d/2)
+ * (Eq.(10)) capped at D+1; after the step stage k_lo retires while
+ * ||dx_k|| <= eps ||x_k|| (relative, reading R34; eps <= 0: 1e3 eps_p with
+ * eps_p = 2^-104, 2^-210, 2^-423) or ||dx_k|| has reached its rounding floor
+ * (<= sqrt(eps_p) ||x_k|| and not below 1/8 of its previous value).  A_0 is factored while stage 0 is active
+ * (x_0 still moves) and reused afterwards (x_0 frozen: the cached factors are
+ * exact); NS_QR_ONCE factors in iteration 1 only.  Exits when all
+ * stages 0..D are retired (converged = 1) or after max_iter iterations.
+ * Synchronises the stream once per iteration (the exit test reads the norms).
+ * log: host [max_iter] or NULL; info: host or NULL.  flags: NS_QR_ONCE |
+ * NS_NO_STAGGER | NS_LEDGER | NS_TILED_BS.  The window is reset to the full
+ * step on return. */
+ns_status ns_run_newton(ns_system* sys, int precision, int dim, int degree, double* x_series, int max_iter,
+                        double eps, uint32_t flags, void* stream, ns_iter_log* log, ns_run_info* info);
 /* Job trace of the last eval/diff (handle created with env NS_TRACE=1): per job
  * [pop, inputs ready, done] globaltimer nanoseconds into host[3*i..], the job
  * descriptors {type, monomial/equation, j, key} into jobs_out[4*i..] (may be

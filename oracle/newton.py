@@ -325,6 +325,57 @@ def step(sys, x_planes, F, split=False):
 
 
 # --------------------------------------------------------------------------
+# staggered computations
+# --------------------------------------------------------------------------
+def staggered_orders(d_max):
+    """The order schedule of Eq.(10): d := d + 1 + d/2 with floor
+    division (reading R19), from d = 1, capped at d_max."""
+    out = [1]
+    while out[-1] < d_max:
+        out.append(min(d_max, out[-1] + 1 + out[-1] // 2))
+    return out
+
+
+def step_window(sys, x_planes, F, k_lo, dc, split=False, x0_factor=None):
+    """One Newton step on the stage window [k_lo, dc): the system
+    is evaluated and differentiated on the series truncated at t^dc (only the
+    coefficients 0..dc-1 are "involved"); the retired stages
+    k < k_lo take dx_k = 0 (Eq.(11): b_k = 0 => dx_k = 0); the
+    active stages solve A_0 dx_k = b_k - sum_{j=1}^{k} A_j dx_{k-j}
+    (Eq.(4)); x_k += dx_k for k < dc, x_k unchanged for k >= dc.  Norms are
+    over k < dc.  ``x0_factor`` (limb planes [K][n][>=1]): factor the A_0 of
+    that earlier x_0 instead (the QR "only once", reused while x_0 is frozen,
+    P:665-668).  Returns the dict of ``step`` (dx and r have dc entries)."""
+    n = sys.n
+    x = read_x(x_planes, F)
+    coeffs = read_coeffs(sys, F)
+    rhs = read_rhs(sys, F)
+    b, A = {}, {}
+    for i in range(n):
+        b[i], A[i] = evaluate_row(sys, x, coeffs, rhs, i, dc, F, split)
+    A0src = A
+    if x0_factor is not None:
+        x0 = read_x(x0_factor[:, :, :1], F)
+        A0src = {i: evaluate_row(sys, x0, coeffs, rhs, i, 1, F, split)[1] for i in range(n)}
+    LU, perm = lu_factor(dense_coeff(A0src, n, 0, F), F)
+    dx = []
+    for k in range(dc):
+        if k < k_lo:
+            dx.append([F.zero] * n)
+            continue
+        rhs_k = [b[i][k] for i in range(n)]
+        for j in range(1, k + 1):
+            Av = matvec_sparse(A, j, dx[k - j], n, F)
+            rhs_k = [rhs_k[i] - Av[i] for i in range(n)]
+        dx.append(lu_solve(LU, perm, rhs_k, F))
+    r = residual(A, b, dx, n, dc, F)
+    x_new = [[x[i][k] + (dx[k][i] if k < dc else F.zero) for k in range(sys.d)] for i in range(n)]
+    bk = [[b[i][k] for i in range(n)] for k in range(dc)]
+    return dict(x=x, b=b, A=A, dx=dx, r=r, x_new=x_new,
+                norm_b=series_norm(bk), norm_r=series_norm(r), norm_dx=series_norm(dx))
+
+
+# --------------------------------------------------------------------------
 # running-error scales (SURVEY.md 8(c) c.4) -- float64 magnitudes only
 # --------------------------------------------------------------------------
 def _absconv(a, b, d):

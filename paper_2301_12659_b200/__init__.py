@@ -23,6 +23,8 @@ NS_REUSE_QR = 1
 NS_NO_RESIDUAL = 2
 NS_LEDGER = 4
 NS_TILED_BS = 8
+NS_QR_ONCE = 16
+NS_NO_STAGGER = 32
 
 STATUS = {0: "NS_OK", 1: "NS_EINVAL", 2: "NS_EPREC", 3: "NS_EDIM", 4: "NS_EMONO", 5: "NS_ESINGULAR",
           6: "NS_ENONFINITE", 7: "NS_ENOMEM", 8: "NS_ECUDA", 9: "NS_ENCCL", 10: "NS_ESTATE"}
@@ -33,7 +35,8 @@ EXPORTS = ["ns_system_create", "ns_system_destroy", "ns_newton_series_step",
            "ns_toeplitz_solve", "ns_get_r_diag", "ns_md_op", "ns_get_status", "ns_get_ledger",
            "ns_reset_ledger", "ns_last_launch_count", "ns_strerror", "ns_build_info",
            "ns_fp64_peak_probe", "ns_md_latency_probe", "ns_barrier_probe", "ns_set_partition",
-           "ns_newton_series_step_from", "ns_get_trace", "ns_get_qr_trace"]
+           "ns_newton_series_step_from", "ns_get_trace", "ns_get_qr_trace", "ns_set_window",
+           "ns_get_stage_norms", "ns_run_newton"]
 
 
 class NSError(RuntimeError):
@@ -51,6 +54,23 @@ class _Desc(ctypes.Structure):
 
 class StepInfo(ctypes.Structure):
     _fields_ = [("status_bits", ctypes.c_uint32), ("qr_cached", ctypes.c_int32)]
+
+
+class IterLog(ctypes.Structure):
+    _fields_ = [("iter", ctypes.c_int32), ("k_lo", ctypes.c_int32), ("dc", ctypes.c_int32), ("qr", ctypes.c_int32),
+                ("norm_b", ctypes.c_double), ("norm_r", ctypes.c_double), ("norm_dx", ctypes.c_double),
+                ("ms", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class RunInfo(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("converged", ctypes.c_int32), ("qr_count", ctypes.c_int32),
+                ("k_lo", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 class Ledger(ctypes.Structure):
@@ -87,6 +107,10 @@ def lib() -> ctypes.CDLL:
         "ns_get_qr_trace": ([vp, vp, i32], i32),
         "ns_newton_series_step_from": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, u32, vp],
                                        ctypes.c_int),
+        "ns_set_window": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+        "ns_get_stage_norms": ([vp, vp], ctypes.c_int),
+        "ns_run_newton": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_double, u32, vp,
+                           ctypes.POINTER(IterLog), ctypes.POINTER(RunInfo)], ctypes.c_int),
         "ns_nnz": ([vp], i32),
         "ns_jacobian_pattern": ([vp, vp, vp], ctypes.c_int),
         "ns_toeplitz_solve": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
@@ -200,6 +224,26 @@ class NewtonSystem:
         _check(lib().ns_newton_series_step_batched(self._h, self.K, self.n, self.D, B, _ptr(x), _ptr(rhs),
                                                    _ptr(residual_out), flags, _stream_ptr(stream)),
                "ns_newton_series_step_batched")
+
+    # ---- staggered Newton (NEXT-1)
+    def set_window(self, k_lo: int, dc: int):
+        """ns_set_window: following steps solve stages [k_lo, dc) on series truncated at t^dc."""
+        _check(lib().ns_set_window(self._h, k_lo, dc), "ns_set_window")
+
+    def stage_norms(self) -> np.ndarray:
+        """ns_get_stage_norms: [4][K][d] md norms sum_i |v_k,i| of b, b - A dx, dx, x (last step)."""
+        out = np.zeros((4, self.K, self.d), np.float64)
+        _check(lib().ns_get_stage_norms(self._h, out.ctypes.data), "ns_get_stage_norms")
+        return out
+
+    def run_newton(self, x, max_iter: int = 24, eps: float = 0.0, flags: int = 0, stream=None):
+        """ns_run_newton: staggered Newton from x (updated in place).  Returns (info, log)."""
+        _require_cuda(x, "x", (self.K, self.n, self.d))
+        log = (IterLog * max(1, max_iter))()
+        info = RunInfo()
+        _check(lib().ns_run_newton(self._h, self.K, self.n, self.D, _ptr(x), max_iter, eps, flags,
+                                   _stream_ptr(stream), log, ctypes.byref(info)), "ns_run_newton")
+        return info.as_dict(), [log[i].as_dict() for i in range(info.iterations)]
 
     # ---- sharded eval/diff (C4)
     def set_partition(self, eq_lo: int, eq_hi: int):

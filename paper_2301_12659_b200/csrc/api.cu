@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -65,7 +66,7 @@ ns_status step_impl(ns_system* s, double* x, double* res_out, uint32_t flags, cu
   CK(cudaEventRecord(s->ev_join, s->side));
   CK(cudaStreamWaitEvent(st, s->ev_join, 0));
   if (ledger) CK(cudaEventRecord(ev[3], st));
-  r = Impl<K>::stage(s, 0, st);
+  r = Impl<K>::stage(s, s->k_lo, st);
   if (r) return r;
   if (ledger) CK(cudaEventRecord(ev[4], st));
   r = Impl<K>::residual(s, x, res_out, st);
@@ -213,6 +214,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   s->n = n;
   s->D = D;
   s->d = D + 1;
+  s->dc = s->d;
   s->K = K;
   s->M = M;
   s->m_max = m_max;
@@ -305,7 +307,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
     ok &= dalloc(&s->part, (size_t)K * n * s->cmax) == cudaSuccess;
   }
   ok &= dalloc(&s->rbuf, (size_t)K * d * n) == cudaSuccess;
-  ok &= dalloc(&s->knorm, (size_t)3 * K * d) == cudaSuccess;
+  ok &= dalloc(&s->knorm, (size_t)4 * K * d) == cudaSuccess;  // |b_k|, |r_k|, |dx_k|, |x_k|
   ok &= dalloc(&s->res_tmp, (size_t)K * 3) == cudaSuccess;
   ok &= dalloc(&s->job_counter, 1) == cudaSuccess;
   ok &= dalloc(&s->bar, 8) == cudaSuccess;
@@ -392,6 +394,7 @@ ns_status ns_newton_series_step_batched(ns_system* s, int precision, int dim, in
   if (precision != s->K) return NS_EPREC;
   if (dim != s->n || degree != s->D || batch < 0 || batch > s->max_batch) return NS_EDIM;
   if (flags & ~(NS_NO_RESIDUAL)) return NS_EINVAL;
+  if (s->k_lo != 0 || s->dc != s->d) return NS_ESTATE;  // the batched kernel runs the full window
   if (batch == 0) return NS_OK;
   cudaStream_t st = (cudaStream_t)stream;
   switch (s->K) {
@@ -491,21 +494,122 @@ ns_status ns_newton_series_step_from(ns_system* s, int precision, int dim, int d
   switch (s->K) {
     case 2:
       if (!(flags & NS_REUSE_QR)) r = Impl<2>::qr(s, s->A0, nullptr, st);
-      if (!r) r = Impl<2>::stage(s, 0, st);
+      if (!r) r = Impl<2>::stage(s, s->k_lo, st);
       if (!r) r = Impl<2>::residual(s, x, res_out, st);
       break;
     case 4:
       if (!(flags & NS_REUSE_QR)) r = Impl<4>::qr(s, s->A0, nullptr, st);
-      if (!r) r = Impl<4>::stage(s, 0, st);
+      if (!r) r = Impl<4>::stage(s, s->k_lo, st);
       if (!r) r = Impl<4>::residual(s, x, res_out, st);
       break;
     default:
       if (!(flags & NS_REUSE_QR)) r = Impl<8>::qr(s, s->A0, nullptr, st);
-      if (!r) r = Impl<8>::stage(s, 0, st);
+      if (!r) r = Impl<8>::stage(s, s->k_lo, st);
       if (!r) r = Impl<8>::residual(s, x, res_out, st);
       break;
   }
   s->last_stream = st;
+  return r;
+}
+
+ns_status ns_set_window(ns_system* s, int k_lo, int dc) {
+  if (!s || k_lo < 0 || dc > s->d || k_lo >= dc) return NS_EINVAL;
+  s->k_lo = k_lo;
+  s->dc = dc;
+  return NS_OK;
+}
+
+ns_status ns_get_stage_norms(ns_system* s, double* out) {
+  if (!s || !out) return NS_EINVAL;
+  CK(cudaSetDevice(s->dev));
+  if (s->last_stream) CK(cudaStreamSynchronize(s->last_stream));
+  else CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out, s->knorm, sizeof(double) * 4 * s->K * s->d, cudaMemcpyDeviceToHost));
+  return NS_OK;
+}
+
+// Staggered Newton driver (include/ns.h).  Host loop:
+// one windowed step per iteration, then the per-stage norms decide the
+// retired stages (reading R34) and the next order (Eq.(10)).
+ns_status ns_run_newton(ns_system* s, int precision, int dim, int degree, double* x, int max_iter, double eps,
+                        uint32_t flags, void* stream, ns_iter_log* log, ns_run_info* info) {
+  if (!s || !x || max_iter < 0) return NS_EINVAL;
+  if (precision != s->K) return NS_EPREC;
+  if (dim != s->n || degree != s->D) return NS_EDIM;
+  if (flags & ~(NS_QR_ONCE | NS_NO_STAGGER | NS_LEDGER | NS_TILED_BS)) return NS_EINVAL;
+  CK(cudaSetDevice(s->dev));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int K = s->K, d = s->d;
+  if (!(eps > 0.0)) eps = 1e3 * std::ldexp(1.0, K == 2 ? -104 : (K == 4 ? -210 : -423));
+  const double sq = std::ldexp(1.0, K == 2 ? -52 : (K == 4 ? -105 : -211));  // sqrt(eps_p)
+  std::vector<double> kn((size_t)4 * K * d), prev(d, HUGE_VAL);  // prev: last ||dx_k|| while active
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  int k_lo = 0, dc = (flags & NS_NO_STAGGER) ? d : 1, qr_count = 0, it = 0;
+  bool converged = false;
+  ns_status r = NS_OK;
+  for (it = 1; it <= max_iter; ++it) {
+    s->k_lo = k_lo;
+    s->dc = dc;
+    const bool refactor = qr_count == 0 || (k_lo == 0 && !(flags & NS_QR_ONCE));
+    uint32_t sf = (flags & (NS_LEDGER | NS_TILED_BS)) | (refactor ? 0u : NS_REUSE_QR);
+    if (!refactor) sf &= ~NS_TILED_BS;  // the cached factorisation keeps its form
+    else s->use_m = !(flags & NS_TILED_BS);
+    if ((r = (cudaEventRecord(e0, st) == cudaSuccess) ? NS_OK : NS_ECUDA)) break;
+    switch (K) {
+      case 2: r = step_impl<2>(s, x, nullptr, sf, st); break;
+      case 4: r = step_impl<4>(s, x, nullptr, sf, st); break;
+      default: r = step_impl<8>(s, x, nullptr, sf, st); break;
+    }
+    if (r) break;
+    if (refactor) ++qr_count;
+    if (cudaEventRecord(e1, st) != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess ||
+        cudaMemcpy(kn.data(), s->knorm, sizeof(double) * kn.size(), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      r = NS_ECUDA;
+      break;
+    }
+    // leading limbs: knorm[w][l][k] at (w * K + l) * d + k
+    auto nrm = [&](int w, int k) { return kn[(size_t)w * K * d + k]; };
+    double nb = 0, nr = 0, ndx = 0;
+    for (int k = 0; k < dc; ++k) {
+      nb = std::max(nb, nrm(0, k));
+      nr = std::max(nr, nrm(1, k));
+      ndx = std::max(ndx, nrm(2, k));
+    }
+    if (log) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      log[it - 1] = ns_iter_log{it, k_lo, dc, refactor ? 1 : 0, nb, nr, ndx, (double)ms};
+    }
+    // retire stage k (reading R34) when its correction is negligible,
+    // ||dx_k|| <= eps ||x_k|| (x_k was already correct, Eq.(11): b_k = 0 =>
+    // dx_k = 0), or when it has reached the rounding floor: below
+    // sqrt(eps_p) ||x_k|| and no longer shrinking (quadratic convergence
+    // would have cut it by far more than 8; late coefficients carry an
+    // amplified floor, kappa_k >> 1, SURVEY c.2 Q26)
+    auto retired = [&](int k) {
+      const double dxk = nrm(2, k), xk = nrm(3, k);
+      if (!std::isfinite(dxk) || !std::isfinite(xk)) return false;
+      if (dxk <= eps * xk) return true;
+      return dxk <= sq * xk && dxk >= prev[k] * 0.125;
+    };
+    while (k_lo < dc && retired(k_lo)) ++k_lo;
+    for (int k = k_lo; k < dc; ++k) prev[k] = nrm(2, k);
+    if (k_lo == d) {
+      converged = true;
+      break;
+    }
+    if (!std::isfinite(nb) || !std::isfinite(ndx)) break;
+    dc = std::min(d, dc + 1 + dc / 2);  // Eq.(10) "d := d + 1 + d/2", floor division
+    if (k_lo >= dc) dc = std::min(d, k_lo + 1);
+  }
+  if (it > max_iter) it = max_iter;
+  s->k_lo = 0;
+  s->dc = d;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (info) *info = ns_run_info{it, converged ? 1 : 0, qr_count, k_lo};
   return r;
 }
 
@@ -528,9 +632,9 @@ ns_status ns_toeplitz_solve(ns_system* s, const double* b, const double* A, cons
   s->last_launches = 0;
   s->use_m = true;
   switch (s->K) {
-    case 2: r = Impl<2>::qr(s, s->A0q, nullptr, st); if (!r) r = Impl<2>::stage(s, 0, st); break;
-    case 4: r = Impl<4>::qr(s, s->A0q, nullptr, st); if (!r) r = Impl<4>::stage(s, 0, st); break;
-    default: r = Impl<8>::qr(s, s->A0q, nullptr, st); if (!r) r = Impl<8>::stage(s, 0, st); break;
+    case 2: r = Impl<2>::qr(s, s->A0q, nullptr, st); if (!r) r = Impl<2>::stage(s, s->k_lo, st); break;
+    case 4: r = Impl<4>::qr(s, s->A0q, nullptr, st); if (!r) r = Impl<4>::stage(s, s->k_lo, st); break;
+    default: r = Impl<8>::qr(s, s->A0q, nullptr, st); if (!r) r = Impl<8>::stage(s, s->k_lo, st); break;
   }
   if (r) return r;
   CK(cudaMemcpyAsync(dx, s->dx, sizeof(double) * K * d * n, cudaMemcpyDeviceToDevice, st));

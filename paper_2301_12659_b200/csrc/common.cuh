@@ -29,6 +29,7 @@ struct DevSys {
   const int* job_order; // [n] equations by decreasing cost (LPT)
   const double* coeff;  // [K][M]
   const double* rhs;    // [K][n][d]
+  int dc;         // active coefficients 0..dc-1 of this step (dc <= d; the staggered window)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {

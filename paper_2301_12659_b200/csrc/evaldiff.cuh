@@ -40,7 +40,9 @@ struct SerRef {
 // the group width G doubles while every lane keeps >= min_terms terms.
 template <int K, typename Get>
 __device__ void conv_batch(int tid, int T, int B, int d, Get get, double* const* c2 = nullptr, int min_terms = 4,
-                           int mode = 0, long long* dbg = nullptr) {
+                           int mode = 0, long long* dbg = nullptr, int ldc = 0) {
+  // d: coefficients computed (the active window's dc); ldc: limb stride of the outputs (0: d)
+  if (ldc == 0) ldc = d;
   const int P = (d + 1) / 2;
   const int groups = B * P;
   // G lanes per coefficient pair; each lane sums >= min_terms of the d+1 terms
@@ -133,11 +135,11 @@ __device__ void conv_batch(int tid, int T, int B, int d, Get get, double* const*
       if (dbg && tid == 0) dbg[1] = clock64();
     }
     if (active && sub == 0) {
-      md::store<K>(c, d, k1, acc1);
-      if (k2 != k1) md::store<K>(c, d, k2, acc2);
+      md::store<K>(c, ldc, k1, acc1);
+      if (k2 != k1) md::store<K>(c, ldc, k2, acc2);
       if (c2) {  // second copy (the chain's pool series next to its smem copy)
-        md::store_cg<K>(c2[bi], d, k1, acc1);
-        if (k2 != k1) md::store_cg<K>(c2[bi], d, k2, acc2);
+        md::store_cg<K>(c2[bi], ldc, k1, acc1);
+        if (k2 != k1) md::store_cg<K>(c2[bi], ldc, k2, acc2);
       }
     }
   }
@@ -264,8 +266,8 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
             pb = SerRef{xbuf[q & 1], d};
             pc = sbuf[q & 1];
           };
-          conv_batch<K>(threadIdx.x, blockDim.x, 1, d, get, &outp, J.conv_terms, J.conv_mode,
-                        (st_tr && q <= 256) ? st_tr + 4 * 256 + 2 * (q - 1) : nullptr);
+          conv_batch<K>(threadIdx.x, blockDim.x, 1, s.dc, get, &outp, J.conv_terms, J.conv_mode,
+                        (st_tr && q <= 256) ? st_tr + 4 * 256 + 2 * (q - 1) : nullptr, d);
           if (st_tr && threadIdx.x == 0 && q <= 256) st_tr[4 * (q - 1) + 1] = clock64();
           cp_async_wait_all();  // the next operand has landed (copy overlapped the convolution)
           __syncthreads();
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
           pb = rb;
           pc = X + (j - 2) * ser;
         };
-        conv_batch<K>(threadIdx.x, blockDim.x, 1, d, get, nullptr, J.conv_terms, J.conv_mode);
+        conv_batch<K>(threadIdx.x, blockDim.x, 1, s.dc, get, nullptr, J.conv_terms, J.conv_mode, nullptr, d);
         __syncthreads();
       }
       if (threadIdx.x == 0) {
@@ -349,13 +351,13 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
       md::mdv<K> c;
 #pragma unroll
       for (int l = 0; l < K; ++l) c.x[l] = s.coeff[(long long)l * s.M + tau];
-      for (int k = threadIdx.x; k < d; k += blockDim.x) {
+      for (int k = threadIdx.x; k < s.dc; k += blockDim.x) {
         md::mdv<K> val = (m == 1) ? md::load<K>(x + (long long)vars[0] * d, xs, k)
                                   : md::load_cg<K>(F + (m - 2) * ser, d, k);
         md::mdv<K> acc = md::load<K>(bacc, d, k);
         md::store<K>(bacc, d, k, md::fma_acc<K>(acc, md::neg<K>(c), val));
       }
-      for (int t = threadIdx.x; t < m * d; t += blockDim.x) {
+      for (int t = threadIdx.x; t < m * s.dc; t += blockDim.x) {
         const int q = t % m, k = t / m;
         md::mdv<K> part;
         if (m == 1) part = md::from_double<K>(k == 0 ? 1.0 : 0.0);

@@ -15,13 +15,18 @@ using ns::DevSys;
 #define dalloc ns_dalloc
 
 namespace {
+// device view of the system; dc = active coefficients of this step (window)
+inline DevSys devsys(const ns_system* s) {
+  return DevSys{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
+                s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs, s->dc};
+}
+
 template <int K>
 ns_status launch_evaldiff(ns_system* s, const double* x, cudaStream_t st) {
   CK(cudaMemsetAsync(s->job_counter, 0, sizeof(int), st));
   CK(cudaMemsetAsync(s->prog, 0, sizeof(int) * 2 * s->M, st));
   CK(cudaMemcpyAsync(s->left, s->left_init, sizeof(int) * s->M, cudaMemcpyDeviceToDevice, st));
-  DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
-            s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
+  DevSys ds = devsys(s);
   ns::EdJobs J{s->jobs, s->njobs, s->ser_off, s->pool, s->prog, s->prog + s->M, s->left, s->trace,
                  s->conv_terms, s->conv_mode};
   ns::evaldiff_jobs_kernel<K><<<s->grid_ed, 256, s->ed_smem, st>>>(ds, J, x, s->b, s->A, s->A0, s->job_counter);
@@ -32,8 +37,7 @@ ns_status launch_evaldiff(ns_system* s, const double* x, cudaStream_t st) {
 
 template <int K>
 ns_status launch_a0(ns_system* s, const double* x, cudaStream_t st) {
-  DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
-            s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
+  DevSys ds = devsys(s);
   const int blocks = std::max(1, std::min(s->sms, (s->n + 3) / 4));
   ns::a0_kernel<K><<<blocks, 128, 0, st>>>(ds, x, s->A0q);
   s->last_launches += 1;
@@ -53,8 +57,7 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
   double *W = s->W, *vh = s->vhead, *be = s->beta, *rd = s->rdiag;
   unsigned *bar = s->bar, *stt = s->status;
   int* fl = s->qr_flags;
-  DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
-            s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
+  DevSys ds = devsys(s);
   const double* xp = x;
   if (s->cqr_on) {
     ns::CqrShape sh{s->cqr_P, s->cqr_W, s->cqr_CPC, s->cqr_RS, (s->cqr_withM && s->use_m) ? 1 : 0};
@@ -112,14 +115,13 @@ template <int K>
 ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
   const int wpb = s->st_threads / 32;
   const int Q = (s->n + wpb - 1) / wpb;
-  if (s->use_m && k_lo == 0 && s->stage_split && Q <= s->grid_st / 2 && s->d >= 3) {
+  if (s->use_m && s->stage_split && Q <= s->grid_st / 2 && s->dc - k_lo >= 3) {
     // split design: critical group + right-looking bulk updates
     CK(cudaMemsetAsync(s->bar + 2, 0, 2 * sizeof(unsigned), st));
     CK(cudaMemsetAsync(s->sflags, 0, sizeof(int) * (2 * s->d + 2), st));
-    DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
-              s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
+    DevSys ds = devsys(s);
     ns::Stage2Args a{s->b, s->A, s->Minv, s->bp, s->dx, s->pend, s->sflags, s->sflags + s->d,
-                     (unsigned*)(s->sflags + 2 * s->d), Q};
+                     (unsigned*)(s->sflags + 2 * s->d), Q, k_lo};
     unsigned* bar = s->bar + 2;
     void* args[] = {&ds, &a, &bar};
     CK(cudaLaunchCooperativeKernel((const void*)ns::stage2_kernel<K>, dim3(s->grid_st), dim3(s->st_threads), args,
@@ -129,8 +131,7 @@ ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
   }
   CK(cudaMemsetAsync(s->bar + 2, 0, 2 * sizeof(unsigned), st));
   CK(cudaMemsetAsync(s->dx, 0, sizeof(double) * (size_t)K * s->d * s->n, st));
-  DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
-            s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
+  DevSys ds = devsys(s);
   ns::StageArgs a{s->b, s->A, s->Qt, s->R, s->invR, s->bp, s->dx, s->y, s->part, s->use_m ? s->Minv : nullptr,
                   s->cmax, s->TB, k_lo};
   unsigned* bar = s->bar + 2;
@@ -143,15 +144,16 @@ ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
 template <int K>
 ns_status launch_residual(ns_system* s, double* x, double* res_out, cudaStream_t st) {
   {
-    const long long rows = (long long)s->d * s->n;
+    const long long rows = (long long)s->dc * s->n;
     const int blocks = (int)std::max<long long>(1, std::min<long long>((rows + 7) / 8, 8LL * s->sms));
-    ns::residual_kernel<K><<<blocks, 256, 0, st>>>(s->n, s->d, 0, s->b, s->bp, s->A0, s->dx, s->rbuf, s->knorm);
-    ns::knorm_kernel<K><<<s->d, 96, 0, st>>>(s->n, s->d, 0, s->b, s->rbuf, s->dx, s->knorm);
+    ns::residual_kernel<K><<<blocks, 256, 0, st>>>(s->n, s->d, s->dc, s->k_lo, s->b, s->bp, s->A0, s->dx, s->rbuf,
+                                                   s->knorm);
+    ns::knorm_kernel<K><<<s->dc, 128, 0, st>>>(s->n, s->d, s->k_lo, s->b, s->rbuf, s->dx, x, s->knorm);
     s->last_launches += 1;
   }
   const long long tot = (long long)s->n * s->d;
   const int blocks = (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, 2LL * s->sms));
-  ns::finalize_kernel<K><<<blocks, 256, 0, st>>>(s->n, s->d, x, s->dx, s->knorm,
+  ns::finalize_kernel<K><<<blocks, 256, 0, st>>>(s->n, s->d, s->dc, x, s->dx, s->knorm,
                                                  res_out ? res_out : s->res_tmp, s->status);
   s->last_launches += 2;
   CK(cudaGetLastError());
@@ -329,8 +331,7 @@ ns_status batched_impl(ns_system* s, int batch, double* x, const double* rhs, do
     if (dalloc(&s->bws, need) != cudaSuccess) return NS_ENOMEM;
     s->bws_per_path = need;
   }
-  DevSys ds{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
-            s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs};
+  DevSys ds = devsys(s);
   ns::batched_step_kernel<K><<<grid, threads, smem_bytes, st>>>(ds, batch, x, rhs, res, s->bws, L, TB);
   s->last_launches = 1;
   s->last_stream = st;

@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(256) stage_kernel(DevSys s, StageArgs a, unsig
   const int TB = a.TB;
   const int T = (n + TB - 1) / TB;
   const long long lsI = (long long)T * TB * TB;
-  for (int k = a.k_lo; k < d; ++k) {
+  for (int k = a.k_lo; k < s.dc; ++k) {
     // ---- updates: b'_k = b_k - sum_{j=1}^{k} A_j dx_{k-j}.  The k*len_i terms
     // of row i are cut into chunks of UCH; (row, chunk) slots are dealt to all
     // warps, each chunk is summed by one warp (fixed lane order + butterfly),
@@ -565,6 +565,7 @@ struct Stage2Args {
   int* pdone;          // [d] rows of pend_k complete
   unsigned* cbar;      // critical-group barrier counter (zeroed per launch)
   int Q;               // CTAs in the critical group
+  int k_lo;            // first active stage (stages below: dx = 0, reading R34); last = s.dc - 1
 };
 
 __device__ __forceinline__ void sub_sync(unsigned* cnt, unsigned& target, unsigned nq) {
@@ -594,13 +595,15 @@ __device__ md::mdv<K> row_dot_A(const DevSys& s, const double* A, int j, const d
 
 template <int K>
 __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, unsigned* bar) {
-  const int n = s.n, d = s.d;
+  const int n = s.n, d = s.d, dc = s.dc, k_lo = a.k_lo;
   const long long lsV = (long long)d * n, lsM = (long long)n * n;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
-  // prologue: pend = b (all CTAs), one full barrier
+  // prologue: pend = b (all CTAs), dx_k = 0 for the retired stages k < k_lo, one full barrier
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)K * d * n;
-       t += (long long)gridDim.x * blockDim.x)
+       t += (long long)gridDim.x * blockDim.x) {
     __stcg(a.pend + t, a.b[t]);
+    if ((int)((t / n) % d) < k_lo) __stcg(a.dx + t, 0.0);
+  }
   {
     GridBarrier gb(bar, 0u);
     gb.sync();
@@ -609,14 +612,14 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
     // ---------------- critical group
     const int cw = blockIdx.x * wpb + wib, ncw = a.Q * wpb;
     unsigned target = 0;
-    for (int k = 0; k < d; ++k) {
-      if (k >= 2) {
+    for (int k = k_lo; k < dc; ++k) {
+      if (k >= k_lo + 2) {
         if (threadIdx.x == 0) flag_wait(a.pdone + k, n);
         __syncthreads();
       }
       for (int i = cw; i < n; i += ncw) {
         md::mdv<K> v = md::load_cg<K>(a.pend + (long long)k * n, lsV, i);
-        if (k >= 1) v = md::sub<K>(v, row_dot_A<K>(s, a.A, 1, a.dx + (long long)(k - 1) * n, lsV, i));
+        if (k >= k_lo + 1) v = md::sub<K>(v, row_dot_A<K>(s, a.A, 1, a.dx + (long long)(k - 1) * n, lsV, i));
         if (lane == 0) md::store_cg<K>(a.bp + (long long)k * n, lsV, i, v);
       }
       sub_sync(a.cbar, target, a.Q);
@@ -632,17 +635,17 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
       if (blockIdx.x == 0 && threadIdx.x == 0) flag_set(a.dxr + k, 1);
     }
   } else {
-    // ---------------- bulk group: (k', i) pairs, k' = 2..d-1, dealt to bulk warps
+    // ---------------- bulk group: (k', i) pairs, k' = k_lo+2..dc-1, dealt to bulk warps
     const int bw = (blockIdx.x - a.Q) * wpb + wib, nbw = ((int)gridDim.x - a.Q) * wpb;
-    const int npairs = (d - 2) * n;
-    for (int k = 0; k + 2 < d; ++k) {
+    const int npairs = (dc - 2 - k_lo) * n;
+    for (int k = k_lo; k + 2 < dc; ++k) {
       bool any = false;
-      for (int p = bw; p < npairs; p += nbw) any |= (2 + p / n >= k + 2);
+      for (int p = bw; p < npairs; p += nbw) any |= (k_lo + 2 + p / n >= k + 2);
       if (!any) break;
       if (lane == 0) flag_wait(a.dxr + k, 1);
       __syncwarp();
       for (int p = bw; p < npairs; p += nbw) {
-        const int kp = 2 + p / n, i = p % n;
+        const int kp = k_lo + 2 + p / n, i = p % n;
         if (kp < k + 2) continue;
         const md::mdv<K> dot = row_dot_A<K>(s, a.A, kp - k, a.dx + (long long)k * n, lsV, i);
         if (lane == 0) {
@@ -660,7 +663,7 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
 // ------------------------------------------------------------------ residual and norms
 // r_k,i = b'_k,i - sum_c A0[i][c] dx_k[c]: warps over all (k, i) rows of the grid.
 template <int K>
-__global__ void __launch_bounds__(256) residual_kernel(int n, int d, int k_lo, const double* __restrict__ b,
+__global__ void __launch_bounds__(256) residual_kernel(int n, int d, int dc, int k_lo, const double* __restrict__ b,
                                                        const double* __restrict__ bp,
                                                        const double* __restrict__ A0,
                                                        const double* __restrict__ dx, double* rbuf,
@@ -668,7 +671,7 @@ __global__ void __launch_bounds__(256) residual_kernel(int n, int d, int k_lo, c
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const long long lsV = (long long)d * n, lsM = (long long)n * n;
-  for (long long row = gw; row < (long long)d * n; row += nw) {
+  for (long long row = gw; row < (long long)dc * n; row += nw) {
     const int k = (int)(row / n), i = (int)(row % n);
     md::mdv<K> acc = md::zero<K>();
     if (k >= k_lo) {
@@ -687,17 +690,18 @@ __global__ void __launch_bounds__(256) residual_kernel(int n, int d, int k_lo, c
   }
 }
 
-// knorm[w][k] = sum_i |v_k,i| for v = b, r, dx (one CTA per k, one warp per norm)
+// knorm[w][k] = sum_i |v_k,i| for v = b, r, dx, x (one CTA per active k, one warp
+// per norm; x is the series before the update, [K][n][d])
 template <int K>
-__global__ void __launch_bounds__(96) knorm_kernel(int n, int d, int k_lo, const double* __restrict__ b,
-                                                   const double* __restrict__ rbuf, const double* __restrict__ dx,
-                                                   double* knorm) {
+__global__ void __launch_bounds__(128) knorm_kernel(int n, int d, int k_lo, const double* __restrict__ b,
+                                                    const double* __restrict__ rbuf, const double* __restrict__ dx,
+                                                    const double* __restrict__ x, double* knorm) {
   const int k = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long lsV = (long long)d * n;
   const double* src = (w == 0) ? b : ((w == 1) ? rbuf : dx);
   md::mdv<K> acc = md::zero<K>();
   for (int i = lane; i < n; i += 32) {
-    md::mdv<K> v = md::load<K>(src + (long long)k * n, lsV, i);
+    md::mdv<K> v = (w == 3) ? md::load<K>(x, lsV, (long long)i * d + k) : md::load<K>(src + (long long)k * n, lsV, i);
     if (w == 2 && k < k_lo) v = md::zero<K>();
     acc = md::add<K>(acc, md::absv<K>(v));
   }
@@ -707,12 +711,13 @@ __global__ void __launch_bounds__(96) knorm_kernel(int n, int d, int k_lo, const
 
 // x += dx (one thread per coefficient); warp 0 of block 0 reduces the norms.
 template <int K>
-__global__ void finalize_kernel(int n, int d, double* x, const double* __restrict__ dx,
+__global__ void finalize_kernel(int n, int d, int dc, double* x, const double* __restrict__ dx,
                                 const double* __restrict__ knorm, double* res_out, unsigned* status) {
   const long long lsX = (long long)n * d, lsV = (long long)d * n;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < (long long)n * d;
        t += (long long)gridDim.x * blockDim.x) {
     const int j = (int)(t / d), k = (int)(t % d);
+    if (k >= dc) continue;  // outside the window: x_k unchanged
     md::mdv<K> xv = md::load<K>(x, lsX, t);
     md::mdv<K> dv = md::load<K>(dx + (long long)k * n, lsV, j);
     md::store<K>(x, lsX, t, md::add<K>(xv, dv));
@@ -722,7 +727,7 @@ __global__ void finalize_kernel(int n, int d, double* x, const double* __restric
     for (int w = 0; w < 3; ++w) {
       md::mdv<K> best = md::zero<K>();
       if (lane == 0) {
-        for (int k = 0; k < d; ++k) {
+        for (int k = 0; k < dc; ++k) {
           md::mdv<K> v = md::load<K>(knorm + (long long)w * K * d, d, k);
           if (md::greater<K>(v, best)) best = v;
         }

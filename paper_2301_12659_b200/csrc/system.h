@@ -10,6 +10,7 @@ struct ns_system {
   int dev = 0;
   int n = 0, D = 0, d = 0, K = 0, M = 0, nnz = 0, m_max = 0, max_batch = 1;
   int TB = 32, T = 1;
+  int k_lo = 0, dc = 0;  // active stage window [k_lo, dc) of the next step (ns_set_window; default [0, d))
   int sms = 0;
   // host copies
   std::vector<int> h_eq_ptr, h_mono_ptr, h_var_idx, h_row_ptr, h_col_idx, h_mono_dst, h_job_order;

@@ -343,3 +343,70 @@ def test_exact_x_is_rounded_closed_form():
         v = sum(Fraction(l) for l in x[:, 1, k])
         want = a ** k / math.factorial(k)
         assert abs(v - want) <= abs(want) * Fraction(2) ** -210
+
+
+# ---------------------------------------------------------------- staggered (NEXT-1)
+def test_staggered_orders_spec_examples():
+    """Eq.(10) with floor division."""
+    assert O.staggered_orders(64) == [1, 2, 4, 7, 11, 17, 26, 40, 61, 64]
+    assert O.staggered_orders(4) == [1, 2, 4]
+    assert O.staggered_orders(1) == [1]
+    assert O.staggered_orders(32) == [1, 2, 4, 7, 11, 17, 26, 32]
+
+
+def test_window_step_prefix_of_full_step():
+    """Truncated products and the block lower-triangular solve: coefficients
+    0..dc-1 of a step on the series truncated at t^dc equal those of the full
+    step (P:495-497 "not all d coefficient vectors need to be involved");
+    x_k, k >= dc, are untouched."""
+    sys_ = synth.triangular_system(4, 6, 2, seed=3)
+    x = synth.make_x(sys_, "near", seed=2)
+    full = O.step(sys_, x, FX)
+    for dc in (1, 3, 7):
+        w = O.step_window(sys_, x, FX, 0, dc)
+        for j in range(4):
+            for k in range(sys_.d):
+                want = full["x_new"][j][k] if k < dc else w["x"][j][k]
+                assert w["x_new"][j][k] == want, (dc, j, k)
+
+
+def test_window_retired_stages_exact_integer_system():
+    """With x_0..x_{k_lo-1} exact, b_k = 0 there exactly, so the full step has
+    dx_k = 0 for k < k_lo (Eq.(11)) and the windowed step [k_lo, d)
+    equals it bit for bit; the retired coefficients stay frozen.  Integer
+    system x_j = 1/(1-t) (exact rational arithmetic)."""
+    sys_ = synth.inv1mt_system(4, 5, 2)
+    x = synth.make_x(sys_, "exact").copy()
+    x[0, :, 3:] += 0.25  # perturb coefficients >= 3 (dyadic, exact)
+    full = O.step(sys_, x, FX)
+    assert all(full["dx"][k][i] == 0 for k in range(3) for i in range(4))
+    w = O.step_window(sys_, x, FX, 3, sys_.d)
+    assert all(w["dx"][k][i] == 0 for k in range(3) for i in range(4))
+    for j in range(4):
+        for k in range(sys_.d):
+            assert w["x_new"][j][k] == full["x_new"][j][k]
+    assert w["norm_r"] == 0
+
+
+def test_staggered_schedule_converges_to_closed_form():
+    """Newton along the staggered schedule from 'start' reaches the
+    closed form exp(alpha t) at every coefficient (quadratic convergence per
+    order step, SURVEY c.3)."""
+    F = O.MPField(600)
+    n, D = 4, 7
+    sys_ = synth.triangular_system(n, D, 8, seed=21)
+    ex = O.read_x(synth.make_x(sys_, "exact"), F)
+    x = synth.make_x(sys_, "start", seed=5)
+    orders = O.staggered_orders(sys_.d) + [sys_.d] * 3
+    for dc in orders:
+        out = O.step_window(sys_, x, F, 0, dc)
+        xs = out["x_new"]
+        # back to limb planes: 8 limbs (2^-424) keep far more than the 2^-380 checked
+        x = np.zeros_like(x)
+        for j in range(n):
+            for k in range(sys_.d):
+                v = F.to_fraction(xs[j][k])
+                num, den = v.numerator, v.denominator
+                x[:, j, k] = synth.rational_to_md(num, den, 8)
+    err = max(abs(F.from_limbs(x[:, j, k]) - ex[j][k]) for j in range(n) for k in range(sys_.d))
+    assert err < F.num(2.0 ** -380), err
