@@ -41,6 +41,8 @@ def parse():
     p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     p.add_argument("--reuse-qr", action="store_true", help="C4: NS_REUSE_QR in the timed steps (QR once)")
     p.add_argument("--batch", type=int, default=4096, help="C5: total paths (partitioned over ranks)")
+    p.add_argument("--driver", action="store_true",
+                   help="NEXT-1: time whole staggered Newton runs (ns_run_newton) from 'start' to convergence")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle work for cpu_baseline")
     return p.parse_args()
@@ -552,8 +554,65 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_driver(args):
+    """NEXT-1: one 'step' = one whole staggered Newton run
+    (ns_run_newton) from the 'start' series (x_0 correct to half
+    precision) until every stage is retired, against the same run
+    with all orders in every iteration (NS_NO_STAGGER).  Device time from
+    CUDA events around each run (the driver synchronises once per iteration
+    to read the norms; that host time is inside the events)."""
+    import torch
+
+    import paper_2301_12659_b200 as P
+    import synth
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    sys_ = synth.build_config(args.config)
+    h = P.NewtonSystem.from_system(sys_, device=local)
+    xs = torch.tensor(synth.make_x(sys_, "start", seed=1), device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out = {}
+    clocks = ClockSampler(local)
+    for name, fl in (("staggered", 0), ("staggered_qr_once", P.NS_QR_ONCE), ("full_orders", P.NS_NO_STAGGER)):
+        for _ in range(max(1, args.warmup)):
+            x = xs.clone()
+            h.run_newton(x, max_iter=24, flags=fl)
+        if name == "staggered":
+            clocks.start()
+        times, info, log = [], None, None
+        for _ in range(args.steps):
+            x = xs.clone()
+            flush.zero_()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            info, log = h.run_newton(x, max_iter=24, flags=fl)
+            b.record()
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        if name == "staggered":
+            clk = clocks.stop()
+        times.sort()
+        out[name] = {"ms_median": times[len(times) // 2], "ms_min": times[0], "iterations": info["iterations"],
+                     "converged": info["converged"], "qr_count": info["qr_count"],
+                     "log": [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in e.items()} for e in log]}
+    line = {"metric": "staggered Newton run ms (ns_run_newton, 'start' to convergence)",
+            "value": out["staggered"]["ms_median"], "unit": "ms", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": False, "dtype": "f64", "data": "synthetic (seeded, synth.py)",
+            "config": {"workload": workload_desc(args.config, sys_).replace("one Newton step", "staggered run"),
+                       "l2": "flushed (256 MiB memset) before every timed run"},
+            "runs": out, "clocks": clk}
+    if rank == 0:
+        print(json.dumps(line))
+
+
 def main():
     args = parse()
+    if args.driver and args.impl == "ours":
+        run_driver(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "C5":

@@ -227,6 +227,11 @@ int32_t ns_get_trace(ns_system* sys, int64_t* host, int32_t capacity_jobs, int32
  * column updated, rows published, reflector j+1 published] into host[8*j..].
  * Synchronises.  Returns the number of steps, -1 without a trace. */
 int32_t ns_get_qr_trace(ns_system* sys, int64_t* host, int32_t capacity_steps);
+/* Stage-chain trace of the last split stage loop (handle created with env
+ * NS_STAGE_TRACE=1): per stage k, 4 globaltimer stamps (ns) of the critical
+ * chain: start, pending rhs complete, b'_k written, dx_k written.  Returns d,
+ * or -1 without a trace. */
+int32_t ns_get_stage_trace(ns_system* sys, int64_t* host_out);
 /* Synchronises; per-class milliseconds accumulated over steps run with NS_LEDGER. */
 ns_status ns_get_ledger(ns_system* sys, ns_ledger* host_out);
 ns_status ns_reset_ledger(ns_system* sys);

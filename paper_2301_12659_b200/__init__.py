@@ -36,7 +36,7 @@ EXPORTS = ["ns_system_create", "ns_system_destroy", "ns_newton_series_step",
            "ns_reset_ledger", "ns_last_launch_count", "ns_strerror", "ns_build_info",
            "ns_fp64_peak_probe", "ns_md_latency_probe", "ns_barrier_probe", "ns_set_partition",
            "ns_newton_series_step_from", "ns_get_trace", "ns_get_qr_trace", "ns_set_window",
-           "ns_get_stage_norms", "ns_run_newton"]
+           "ns_get_stage_norms", "ns_run_newton", "ns_get_stage_trace"]
 
 
 class NSError(RuntimeError):
@@ -105,6 +105,7 @@ def lib() -> ctypes.CDLL:
         "ns_set_partition": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "ns_get_trace": ([vp, vp, i32, vp], i32),
         "ns_get_qr_trace": ([vp, vp, i32], i32),
+        "ns_get_stage_trace": ([vp, vp], i32),
         "ns_newton_series_step_from": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, u32, vp],
                                        ctypes.c_int),
         "ns_set_window": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
@@ -318,6 +319,13 @@ class NewtonSystem:
         if nj < 0:
             raise RuntimeError("no trace (create the handle with NS_TRACE=1)")
         return t[:nj], jb[:nj]
+
+    def stage_trace(self):
+        """Critical-chain stamps of the last split stage loop (env NS_STAGE_TRACE=1 at create): [d][4] ns."""
+        t = np.zeros((self.d, 4), np.int64)
+        if int(lib().ns_get_stage_trace(self._h, t.ctypes.data)) < 0:
+            raise RuntimeError("no stage trace (create the handle with NS_STAGE_TRACE=1)")
+        return t
 
     def last_launch_count(self) -> int:
         return int(lib().ns_last_launch_count(self._h))

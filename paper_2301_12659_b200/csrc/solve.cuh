@@ -548,12 +548,18 @@ __global__ void __launch_bounds__(256) stage_kernel(DevSys s, StageArgs a, unsig
 // ------------------------------------------------------------------ stage loop, split design
 // Right-looking updates off the critical path.  CTAs [0, Q) (the critical
 // group, one warp per row) run the dependent chain
-//   b'_k = pend_k - A_1 dx_{k-1};  sub-barrier;  dx_k = M b'_k;  sub-barrier;  publish dx_k
+//   b'_k = pend_k - A_1 dx_{k-1};  sub-barrier;  dx_k = M b'_k;
+//   sub-barrier;  publish dx_k (counter ndx = k + 1)
 // while CTAs [Q, G) (the bulk group) apply, as soon as dx_k is published,
-//   pend_{k'} -= A_{k'-k} dx_k   for every k' >= k + 2, every row,
-// each (k', row) pair owned by one bulk warp that takes k = 0, 1, ... in order,
-// so pend_{k'} = b_{k'} - sum_{j >= 2} A_j dx_{k'-j} accumulates in a fixed
-// order (deterministic).  pdone[k'] counts rows whose pend_{k'} is complete.
+//   pend_{k'} -= A_{k'-k} dx_k   for every k' >= k + 2, every row.
+// Each (k', row) pair is owned by one bulk warp (lane-held, up to 32 per
+// group) that applies k = k_lo, k_lo+1, ... in order, so
+// pend_{k'} = b_{k'} - sum_{j >= 2} A_j dx_{k'-j} accumulates in a fixed order
+// (deterministic) whatever the timing; among its pairs with work available
+// the warp always takes the most urgent (smallest k').  (Moving the j = 2
+// term into the critical chain too was measured slower: the chain's row dots
+// are FP64-issue bound, NS_STAGE_TRACE.)
+// pdone[k'] counts rows whose pend_{k'} is complete.
 struct Stage2Args {
   const double* b;     // [K][d][n]
   const double* A;     // [K][d][nnz]
@@ -561,11 +567,12 @@ struct Stage2Args {
   double* bp;          // [K][d][n]   b'_k
   double* dx;          // [K][d][n]
   double* pend;        // [K][d][n]   pending right-hand sides
-  int* dxr;            // [d] dx_k published (0/1, zeroed per launch)
+  int* ndx;            // [1] dx_0..dx_{ndx-1} published (zeroed per launch)
   int* pdone;          // [d] rows of pend_k complete
   unsigned* cbar;      // critical-group barrier counter (zeroed per launch)
   int Q;               // CTAs in the critical group
   int k_lo;            // first active stage (stages below: dx = 0, reading R34); last = s.dc - 1
+  long long* tr;       // [d][4] globaltimer stamps of the critical chain (NS_STAGE_TRACE), or nullptr
 };
 
 __device__ __forceinline__ void sub_sync(unsigned* cnt, unsigned& target, unsigned nq) {
@@ -612,17 +619,22 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
     // ---------------- critical group
     const int cw = blockIdx.x * wpb + wib, ncw = a.Q * wpb;
     unsigned target = 0;
+    const bool trc = a.tr && blockIdx.x == 0 && threadIdx.x == 0;
     for (int k = k_lo; k < dc; ++k) {
+      if (trc) a.tr[4 * k] = gtimer();
       if (k >= k_lo + 2) {
         if (threadIdx.x == 0) flag_wait(a.pdone + k, n);
         __syncthreads();
       }
+      if (trc) a.tr[4 * k + 1] = gtimer();
       for (int i = cw; i < n; i += ncw) {
         md::mdv<K> v = md::load_cg<K>(a.pend + (long long)k * n, lsV, i);
-        if (k >= k_lo + 1) v = md::sub<K>(v, row_dot_A<K>(s, a.A, 1, a.dx + (long long)(k - 1) * n, lsV, i));
+        if (k >= k_lo + 1)
+          v = md::sub<K>(v, row_dot_A<K>(s, a.A, 1, a.dx + (long long)(k - 1) * n, lsV, i));
         if (lane == 0) md::store_cg<K>(a.bp + (long long)k * n, lsV, i, v);
       }
       sub_sync(a.cbar, target, a.Q);
+      if (trc) a.tr[4 * k + 2] = gtimer();
       for (int r = cw; r < n; r += ncw) {
         md::mdv<K> acc = md::dot_ilp<K, 1>(lane, n, 32, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
           xa = md::load<K>(a.M, lsM, (long long)r * n + c);
@@ -632,28 +644,46 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
         if (lane == 0) md::store_cg<K>(a.dx + (long long)k * n, lsV, r, acc);
       }
       sub_sync(a.cbar, target, a.Q);
-      if (blockIdx.x == 0 && threadIdx.x == 0) flag_set(a.dxr + k, 1);
+      if (trc) a.tr[4 * k + 3] = gtimer();
+      if (blockIdx.x == 0 && threadIdx.x == 0) flag_set(a.ndx, k + 1);
     }
   } else {
-    // ---------------- bulk group: (k', i) pairs, k' = k_lo+2..dc-1, dealt to bulk warps
+    // ---------------- bulk group: (k', i) pairs, k' = k_lo+2..dc-1; a warp holds up to 32
+    // pairs (one per lane, ascending k') and always serves the most urgent one with work
     const int bw = (blockIdx.x - a.Q) * wpb + wib, nbw = ((int)gridDim.x - a.Q) * wpb;
     const int npairs = (dc - 2 - k_lo) * n;
-    for (int k = k_lo; k + 2 < dc; ++k) {
-      bool any = false;
-      for (int p = bw; p < npairs; p += nbw) any |= (k_lo + 2 + p / n >= k + 2);
-      if (!any) break;
-      if (lane == 0) flag_wait(a.dxr + k, 1);
-      __syncwarp();
-      for (int p = bw; p < npairs; p += nbw) {
-        const int kp = k_lo + 2 + p / n, i = p % n;
-        if (kp < k + 2) continue;
-        const md::mdv<K> dot = row_dot_A<K>(s, a.A, kp - k, a.dx + (long long)k * n, lsV, i);
-        if (lane == 0) {
-          const long long e = (long long)kp * n;
-          md::store_cg<K>(a.pend + e, lsV, i, md::sub<K>(md::load_cg<K>(a.pend + e, lsV, i), dot));
-          if (k == kp - 2) {  // last contribution to pend_{k'} row i
-            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.pdone + kp) : "memory");
+    int avail = 0;  // dx published so far (this warp's view)
+    for (int g0 = bw; g0 < npairs; g0 += 32 * nbw) {
+      const int p = g0 + lane * nbw;
+      const bool has = p < npairs;
+      const int kp = has ? k_lo + 2 + p / n : 0, i = has ? p % n : 0;
+      int pk = k_lo;  // next dx_k to apply to pend_{kp} row i; complete after k = kp - 2
+      bool live = has;
+      for (;;) {
+        if (!__any_sync(0xffffffffu, live)) break;
+        const unsigned m = __ballot_sync(0xffffffffu, live && pk < avail);
+        if (m == 0) {  // nothing available: wait for the next dx
+          if (lane == 0) {
+            while (ld_relaxed_s32(a.ndx) <= avail) {
+            }
+            avail = ld_acquire(a.ndx);
           }
+          avail = __shfl_sync(0xffffffffu, avail, 0);
+          continue;
+        }
+        const int src = __ffs(m) - 1;
+        const int skp = __shfl_sync(0xffffffffu, kp, src), si = __shfl_sync(0xffffffffu, i, src);
+        const int spk = __shfl_sync(0xffffffffu, pk, src);
+        const md::mdv<K> dot = row_dot_A<K>(s, a.A, skp - spk, a.dx + (long long)spk * n, lsV, si);
+        if (lane == 0) {
+          const long long e = (long long)skp * n;
+          md::store_cg<K>(a.pend + e, lsV, si, md::sub<K>(md::load_cg<K>(a.pend + e, lsV, si), dot));
+          if (spk == skp - 2)  // last contribution to pend_{k'} row i
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.pdone + skp) : "memory");
+        }
+        if (lane == src) {
+          ++pk;
+          live = pk <= kp - 2;
         }
       }
     }

@@ -37,11 +37,13 @@ struct ns_system {
   int* left = nullptr;       // [M]
   int* left_init = nullptr;  // [M]
   long long* trace = nullptr;  // [njobs][3] job trace (NS_TRACE=1 at create), else nullptr
+  long long* strace = nullptr; // [d][4] stage-chain stamps (NS_STAGE_TRACE=1 at create), else nullptr
   unsigned* bar = nullptr;     // [4]: qr barrier, stage barrier
   unsigned* status = nullptr;  // device status word
   int grid_ed = 0, grid_qr = 0, grid_st = 0;
   size_t qr_smem_reserve = 0;
   int st_threads = 256;        // threads per CTA of the stage kernel
+  int st2_threads = 64, grid_st2 = 0;  // split stage kernel (stage2_kernel): CTA size and grid
   int qr_threads = 128;        // threads per CTA of the QR kernel
   bool cqr_on = false;         // cluster QR (cqr.cuh) instead of householder_qr_kernel
   int cqr_P = 0, cqr_W = 0, cqr_CPC = 0, cqr_RS = 0, cqr_E = 0;
