@@ -620,6 +620,32 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
     const int cw = blockIdx.x * wpb + wib, ncw = a.Q * wpb;
     unsigned target = 0;
     const bool trc = a.tr && blockIdx.x == 0 && threadIdx.x == 0;
+    // Each critical warp owns at most one row (ncw >= n).  The stage-invariant
+    // operands of its two dots -- row i of A_1 with its column indices and row
+    // i of M -- stay in registers for the whole loop (lane l holds entries
+    // l + 32 q), so a stage only loads dx_{k-1} and b'_k.  Same term order as
+    // the streamed path (dot_ilp<K, 1>), so the results are identical.
+    // (not at 8d: the cached operands cost spills there; C3 measured 22 vs 17 us per dot)
+    constexpr int RQ = 2;  // n <= 64 (C2)
+    const int row = cw;
+    int r0 = 0, len = 0;
+    if (row < n) {
+      r0 = s.row_ptr[row];
+      len = s.row_ptr[row + 1] - r0;
+    }
+    const bool cache = K < 8 && row < n && n <= 32 * RQ && len <= 32 * RQ;  // warp-uniform
+    md::mdv<K> a1c[RQ], mc[RQ];
+    int colc[RQ];
+    if (cache) {
+      const long long lsA = (long long)d * s.nnz;
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) {
+        const int t = lane + 32 * q;
+        a1c[q] = (t < len) ? md::load<K>(a.A + s.nnz, lsA, r0 + t) : md::zero<K>();
+        colc[q] = (t < len) ? s.col_idx[r0 + t] : 0;
+        mc[q] = (t < n) ? md::load<K>(a.M, lsM, (long long)row * n + t) : md::zero<K>();
+      }
+    }
     for (int k = k_lo; k < dc; ++k) {
       if (trc) a.tr[4 * k] = gtimer();
       if (k >= k_lo + 2) {
@@ -627,6 +653,37 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
         __syncthreads();
       }
       if (trc) a.tr[4 * k + 1] = gtimer();
+      if (cache) {
+        md::mdv<K> v = md::load_cg<K>(a.pend + (long long)k * n, lsV, row);
+        if (k >= k_lo + 1) {
+          const double* xp = a.dx + (long long)(k - 1) * n;
+          md::mdv<K> xv[RQ];
+#pragma unroll
+          for (int q = 0; q < RQ; ++q) xv[q] = (lane + 32 * q < len) ? md::load_cg<K>(xp, lsV, colc[q]) : md::zero<K>();
+          md::mdv<K> p = md::zero<K>();
+#pragma unroll
+          for (int q = 0; q < RQ; ++q)
+            if (lane + 32 * q < len) p = md::fma_acc<K>(p, a1c[q], xv[q]);
+          v = md::sub<K>(v, md::group_sum<K>(p, 32));
+        }
+        if (lane == 0) md::store_cg<K>(a.bp + (long long)k * n, lsV, row, v);
+        sub_sync(a.cbar, target, a.Q);
+        if (trc) a.tr[4 * k + 2] = gtimer();
+        const double* bk = a.bp + (long long)k * n;
+        md::mdv<K> bv[RQ];
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) bv[q] = (lane + 32 * q < n) ? md::load_cg<K>(bk, lsV, lane + 32 * q) : md::zero<K>();
+        md::mdv<K> acc = md::zero<K>();
+#pragma unroll
+        for (int q = 0; q < RQ; ++q)
+          if (lane + 32 * q < n) acc = md::fma_acc<K>(acc, mc[q], bv[q]);
+        acc = md::group_sum<K>(acc, 32);
+        if (lane == 0) md::store_cg<K>(a.dx + (long long)k * n, lsV, row, acc);
+        sub_sync(a.cbar, target, a.Q);
+        if (trc) a.tr[4 * k + 3] = gtimer();
+        if (blockIdx.x == 0 && threadIdx.x == 0) flag_set(a.ndx, k + 1);
+        continue;
+      }
       for (int i = cw; i < n; i += ncw) {
         md::mdv<K> v = md::load_cg<K>(a.pend + (long long)k * n, lsV, i);
         if (k >= k_lo + 1)
@@ -752,18 +809,26 @@ __global__ void finalize_kernel(int n, int d, int dc, double* x, const double* _
     md::mdv<K> dv = md::load<K>(dx + (long long)k * n, lsV, j);
     md::store<K>(x, lsX, t, md::add<K>(xv, dv));
   }
-  if (blockIdx.x == 0 && threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    for (int w = 0; w < 3; ++w) {
-      md::mdv<K> best = md::zero<K>();
-      if (lane == 0) {
-        for (int k = 0; k < dc; ++k) {
-          md::mdv<K> v = md::load<K>(knorm + (long long)w * K * d, d, k);
-          if (md::greater<K>(v, best)) best = v;
-        }
-        md::store<K>(res_out, 3, w, best);
-        if (!isfinite(best.x[0])) atomicOr(status, ST_NONFINITE);
-      }
+  if (blockIdx.x == 0 && threadIdx.x < 96) {
+    // warp w: max over k of knorm[w][k]; lanes stride k, then a shuffle max
+    // (a max is exact, so the order does not matter)
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    md::mdv<K> best = md::zero<K>();
+    bool nonfinite = false;
+    for (int k = lane; k < dc; k += 32) {
+      const md::mdv<K> v = md::load<K>(knorm + (long long)w * K * d, d, k);
+      nonfinite |= !isfinite(v.x[0]);
+      if (md::greater<K>(v, best)) best = v;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const md::mdv<K> o = md::shfl_xor<K>(best, off);
+      if (md::greater<K>(o, best)) best = o;
+    }
+    nonfinite = __any_sync(0xffffffffu, nonfinite);
+    if (lane == 0) {
+      md::store<K>(res_out, 3, w, best);
+      if (nonfinite || !isfinite(best.x[0])) atomicOr(status, ST_NONFINITE);
     }
   }
 }
