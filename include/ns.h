@@ -194,6 +194,20 @@ ns_status ns_get_status(ns_system* sys, ns_step_info* host_out);
  * Host-side state; stream-ordered with the steps that follow. */
 ns_status ns_set_window(ns_system* sys, int k_lo, int dc);
 
+/* Residual sampling (NEXT-4: "select at random one or a couple
+ * of equations and compute the residuals for those selected equations"):
+ * following steps compute r_k,i = b'_k,i - (A_0 dx_k)_i only for the count
+ * distinct equations rows[0..count) (host array, each < dim), and ||r|| is
+ * max_k sum over those rows.  count = 0 restores all equations.  NS_EINVAL
+ * for a repeated or out-of-range row.  Synchronises the device (upload). */
+ns_status ns_set_residual_sample(ns_system* sys, const int32_t* rows, int count);
+
+/* Fabry ratios (NEXT-4; Theorem 1, numerical interpretation
+ * P:210-219): z[K][dim] (device) = c_{D-1} / c_D of each series x_j of
+ * x_series (device [K][dim][D+1]); |z_j| estimates the radius of convergence.
+ * c_D = 0 gives +inf.  NS_EINVAL for degree 0.  Asynchronous on stream. */
+ns_status ns_fabry_ratio(ns_system* sys, const double* x_series, double* z, void* stream);
+
 /* Per-stage norms of the last step (synchronises its stream): host_out
  * [4][K][D+1] md values sum_i |v_k,i| for v = b, b - A dx, dx and x (x before
  * the update); entries k >= dc of the last window are stale. */

@@ -376,6 +376,27 @@ def step_window(sys, x_planes, F, k_lo, dc, split=False, x0_factor=None):
 
 
 # --------------------------------------------------------------------------
+# NEXT-4: residual sampling and the Fabry ratio
+# --------------------------------------------------------------------------
+def residual_norm_sampled(r, rows):
+    """||r|| over the selected equations only: max over k of sum_{i in rows}
+    |r_k,i| ("compute the residuals for those selected equations", P:918-921;
+    norm of reading R16)."""
+    return max(sum(abs(rk[i]) for i in rows) for rk in r)
+
+
+def fabry_ratio(series, F):
+    """c_{d-2} / c_{d-1} of a series with d coefficients: the ratio of
+    Theorem 1 (Fabry) at the last two computed coefficients, an
+    estimate of the nearest singular point z (radius |z|).  None
+    when c_{d-1} = 0."""
+    c_last = series[-1]
+    if c_last == 0:
+        return None
+    return series[-2] / c_last
+
+
+# --------------------------------------------------------------------------
 # running-error scales (SURVEY.md 8(c) c.4) -- float64 magnitudes only
 # --------------------------------------------------------------------------
 def _absconv(a, b, d):

@@ -36,7 +36,8 @@ EXPORTS = ["ns_system_create", "ns_system_destroy", "ns_newton_series_step",
            "ns_reset_ledger", "ns_last_launch_count", "ns_strerror", "ns_build_info",
            "ns_fp64_peak_probe", "ns_md_latency_probe", "ns_barrier_probe", "ns_set_partition",
            "ns_newton_series_step_from", "ns_get_trace", "ns_get_qr_trace", "ns_set_window",
-           "ns_get_stage_norms", "ns_run_newton", "ns_get_stage_trace"]
+           "ns_get_stage_norms", "ns_run_newton", "ns_get_stage_trace",
+           "ns_set_residual_sample", "ns_fabry_ratio"]
 
 
 class NSError(RuntimeError):
@@ -106,6 +107,8 @@ def lib() -> ctypes.CDLL:
         "ns_get_trace": ([vp, vp, i32, vp], i32),
         "ns_get_qr_trace": ([vp, vp, i32], i32),
         "ns_get_stage_trace": ([vp, vp], i32),
+        "ns_set_residual_sample": ([vp, vp, ctypes.c_int], ctypes.c_int),
+        "ns_fabry_ratio": ([vp, vp, vp, vp], ctypes.c_int),
         "ns_newton_series_step_from": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, u32, vp],
                                        ctypes.c_int),
         "ns_set_window": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
@@ -245,6 +248,21 @@ class NewtonSystem:
         _check(lib().ns_run_newton(self._h, self.K, self.n, self.D, _ptr(x), max_iter, eps, flags,
                                    _stream_ptr(stream), log, ctypes.byref(info)), "ns_run_newton")
         return info.as_dict(), [log[i].as_dict() for i in range(info.iterations)]
+
+    # ---- NEXT-4: residual sampling and Fabry ratios
+    def set_residual_sample(self, rows=None):
+        """ns_set_residual_sample: residuals of the listed equations only (None/empty: all)."""
+        r = np.ascontiguousarray([] if rows is None else rows, np.int32)
+        _check(lib().ns_set_residual_sample(self._h, r.ctypes.data if len(r) else None, len(r)),
+               "ns_set_residual_sample")
+
+    def fabry_ratio(self, x, stream=None):
+        """ns_fabry_ratio: z [K][n] = c_{D-1} / c_D per series of x."""
+        import torch
+        _require_cuda(x, "x", (self.K, self.n, self.d))
+        z = torch.empty((self.K, self.n), dtype=torch.float64, device=x.device)
+        _check(lib().ns_fabry_ratio(self._h, _ptr(x), _ptr(z), _stream_ptr(stream)), "ns_fabry_ratio")
+        return z
 
     # ---- sharded eval/diff (C4)
     def set_partition(self, eq_lo: int, eq_hi: int):

@@ -113,7 +113,7 @@ void free_all(ns_system* s) {
                   s->coeff, s->rhs, s->b, s->A, s->A0, s->W, s->vhead, s->beta, s->rdiag, s->R, s->Qt,
                   s->invR, s->bp, s->dx, s->y, s->part, s->Minv, s->Z, s->pend, s->sflags, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
                   s->bar, s->status, s->bws, s->A0q, s->qr_flags, s->jobs, s->ser_off, s->pool, s->prog, s->left,
-                  s->left_init, s->trace, s->strace};
+                  s->left_init, s->trace, s->strace, s->sample_rows};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& row : s->ev)
@@ -526,6 +526,36 @@ ns_status ns_set_window(ns_system* s, int k_lo, int dc) {
   s->k_lo = k_lo;
   s->dc = dc;
   return NS_OK;
+}
+
+ns_status ns_set_residual_sample(ns_system* s, const int32_t* rows, int count) {
+  if (!s || count < 0 || count > s->n || (count > 0 && !rows)) return NS_EINVAL;
+  if (count == 0) {
+    s->n_sample = 0;
+    return NS_OK;
+  }
+  std::vector<char> seen(s->n, 0);
+  for (int t = 0; t < count; ++t) {
+    if (rows[t] < 0 || rows[t] >= s->n || seen[rows[t]]) return NS_EINVAL;
+    seen[rows[t]] = 1;
+  }
+  CK(cudaSetDevice(s->dev));
+  if (!s->sample_rows && dalloc(&s->sample_rows, (size_t)s->n) != cudaSuccess) return NS_ENOMEM;
+  // synchronous upload: steps already queued keep their sample (host-side state)
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(s->sample_rows, rows, sizeof(int32_t) * count, cudaMemcpyHostToDevice));
+  s->n_sample = count;
+  return NS_OK;
+}
+
+ns_status ns_fabry_ratio(ns_system* s, const double* x, double* z, void* stream) {
+  if (!s || !x || !z || s->d < 2) return NS_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (s->K) {
+    case 2: return Impl<2>::fabry(s, x, z, st);
+    case 4: return Impl<4>::fabry(s, x, z, st);
+    default: return Impl<8>::fabry(s, x, z, st);
+  }
 }
 
 ns_status ns_get_stage_norms(ns_system* s, double* out) {

@@ -144,11 +144,13 @@ ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
 template <int K>
 ns_status launch_residual(ns_system* s, double* x, double* res_out, cudaStream_t st) {
   {
-    const long long rows = (long long)s->dc * s->n;
+    const int nr = s->n_sample ? s->n_sample : s->n;
+    const int* rl = s->n_sample ? s->sample_rows : nullptr;
+    const long long rows = (long long)s->dc * nr;
     const int blocks = (int)std::max<long long>(1, std::min<long long>((rows + 7) / 8, 8LL * s->sms));
-    ns::residual_kernel<K><<<blocks, 256, 0, st>>>(s->n, s->d, s->dc, s->k_lo, s->b, s->bp, s->A0, s->dx, s->rbuf,
-                                                   s->knorm);
-    ns::knorm_kernel<K><<<s->dc, 128, 0, st>>>(s->n, s->d, s->k_lo, s->b, s->rbuf, s->dx, x, s->knorm);
+    ns::residual_kernel<K><<<blocks, 256, 0, st>>>(s->n, s->d, s->dc, s->k_lo, rl, nr, s->b, s->bp, s->A0, s->dx,
+                                                   s->rbuf, s->knorm);
+    ns::knorm_kernel<K><<<s->dc, 128, 0, st>>>(s->n, s->d, s->k_lo, rl, nr, s->b, s->rbuf, s->dx, x, s->knorm);
     s->last_launches += 1;
   }
   const long long tot = (long long)s->n * s->d;
@@ -425,6 +427,11 @@ ns_status Impl<K>::stage(ns_system* s, int k_lo, cudaStream_t st) { return launc
 template <int K>
 ns_status Impl<K>::residual(ns_system* s, double* x, double* r, cudaStream_t st) {
   return launch_residual<K>(s, x, r, st);
+}
+template <int K>
+ns_status Impl<K>::fabry(ns_system* s, const double* x, double* z, cudaStream_t st) {
+  ns::fabry_kernel<K><<<(s->n + 127) / 128, 128, 0, st>>>(s->n, s->d, x, z);
+  return cudaGetLastError() == cudaSuccess ? NS_OK : NS_ECUDA;
 }
 template <int K>
 ns_status Impl<K>::batched(ns_system* s, int batch, double* x, const double* rhs, double* res, uint32_t flags,

@@ -750,7 +750,8 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
 // ------------------------------------------------------------------ residual and norms
 // r_k,i = b'_k,i - sum_c A0[i][c] dx_k[c]: warps over all (k, i) rows of the grid.
 template <int K>
-__global__ void __launch_bounds__(256) residual_kernel(int n, int d, int dc, int k_lo, const double* __restrict__ b,
+__global__ void __launch_bounds__(256) residual_kernel(int n, int d, int dc, int k_lo, const int* __restrict__ rows,
+                                                       int nr, const double* __restrict__ b,
                                                        const double* __restrict__ bp,
                                                        const double* __restrict__ A0,
                                                        const double* __restrict__ dx, double* rbuf,
@@ -758,8 +759,9 @@ __global__ void __launch_bounds__(256) residual_kernel(int n, int d, int dc, int
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const long long lsV = (long long)d * n, lsM = (long long)n * n;
-  for (long long row = gw; row < (long long)dc * n; row += nw) {
-    const int k = (int)(row / n), i = (int)(row % n);
+  // rows: the sampled equations (NEXT-4), nr of them; nullptr = all n
+  for (long long row = gw; row < (long long)dc * nr; row += nw) {
+    const int k = (int)(row / nr), i = rows ? rows[row % nr] : (int)(row % nr);
     md::mdv<K> acc = md::zero<K>();
     if (k >= k_lo) {
       for (int c = lane; c < n; c += 32) {
@@ -780,20 +782,43 @@ __global__ void __launch_bounds__(256) residual_kernel(int n, int d, int dc, int
 // knorm[w][k] = sum_i |v_k,i| for v = b, r, dx, x (one CTA per active k, one warp
 // per norm; x is the series before the update, [K][n][d])
 template <int K>
-__global__ void __launch_bounds__(128) knorm_kernel(int n, int d, int k_lo, const double* __restrict__ b,
+__global__ void __launch_bounds__(128) knorm_kernel(int n, int d, int k_lo, const int* __restrict__ rows, int nr,
+                                                    const double* __restrict__ b,
                                                     const double* __restrict__ rbuf, const double* __restrict__ dx,
                                                     const double* __restrict__ x, double* knorm) {
   const int k = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long lsV = (long long)d * n;
   const double* src = (w == 0) ? b : ((w == 1) ? rbuf : dx);
   md::mdv<K> acc = md::zero<K>();
-  for (int i = lane; i < n; i += 32) {
+  const int cnt = (w == 1) ? nr : n;  // the residual norm runs over the sampled equations
+  for (int t = lane; t < cnt; t += 32) {
+    const int i = (w == 1 && rows) ? rows[t] : t;
     md::mdv<K> v = (w == 3) ? md::load<K>(x, lsV, (long long)i * d + k) : md::load<K>(src + (long long)k * n, lsV, i);
     if (w == 2 && k < k_lo) v = md::zero<K>();
     acc = md::add<K>(acc, md::absv<K>(v));
   }
   acc = md::group_sum<K>(acc, 32);
   if (lane == 0) md::store<K>(knorm + (long long)w * K * d, d, k, acc);
+}
+
+// Fabry ratio (NEXT-4; Theorem 1 P:194-208 and its numerical interpretation
+// P:210-219): z_j = c_{D-1} / c_D of the series x_j, an estimate of the
+// nearest singularity (|z_j| = radius of convergence); c_D = 0 gives +inf.
+template <int K>
+__global__ void fabry_kernel(int n, int d, const double* __restrict__ x, double* z) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const long long lsX = (long long)n * d;
+  const md::mdv<K> a = md::load<K>(x, lsX, (long long)j * d + d - 2);
+  const md::mdv<K> c = md::load<K>(x, lsX, (long long)j * d + d - 1);
+  md::mdv<K> r;
+  if (md::is_zero<K>(c)) {
+    r = md::zero<K>();
+    r.x[0] = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+  } else {
+    r = md::div<K>(a, c);
+  }
+  md::store<K>(z, n, j, r);
 }
 
 // x += dx (one thread per coefficient); warp 0 of block 0 reduces the norms.

@@ -10,7 +10,9 @@ struct ns_system {
   int dev = 0;
   int n = 0, D = 0, d = 0, K = 0, M = 0, nnz = 0, m_max = 0, max_batch = 1;
   int TB = 32, T = 1;
-  int k_lo = 0, dc = 0;  // active stage window [k_lo, dc) of the next step (ns_set_window; default [0, d))
+  int k_lo = 0, dc = 0;
+  int n_sample = 0;              // residual sampling (ns_set_residual_sample): 0 = all equations
+  int* sample_rows = nullptr;    // [n] device list of the sampled equations  // active stage window [k_lo, dc) of the next step (ns_set_window; default [0, d))
   int sms = 0;
   // host copies
   std::vector<int> h_eq_ptr, h_mono_ptr, h_var_idx, h_row_ptr, h_col_idx, h_mono_dst, h_job_order;
@@ -86,6 +88,7 @@ struct Impl {
   static ns_status a0(ns_system* s, const double* x, cudaStream_t st);
   static ns_status stage(ns_system* s, int k_lo, cudaStream_t st);
   static ns_status residual(ns_system* s, double* x, double* res_out, cudaStream_t st);
+  static ns_status fabry(ns_system* s, const double* x, double* z, cudaStream_t st);
   static ns_status batched(ns_system* s, int batch, double* x, const double* rhs, double* res,
                            uint32_t flags, cudaStream_t st);
   static ns_status md_op(int op, int n, const double* a, const double* b, double* c, cudaStream_t st);

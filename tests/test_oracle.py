@@ -410,3 +410,40 @@ def test_staggered_schedule_converges_to_closed_form():
                 x[:, j, k] = synth.rational_to_md(num, den, 8)
     err = max(abs(F.from_limbs(x[:, j, k]) - ex[j][k]) for j in range(n) for k in range(sys_.d))
     assert err < F.num(2.0 ** -380), err
+
+
+# ---------------------------------------------------------------- NEXT-4
+def test_fabry_ratio_closed_forms():
+    """Theorem 1: x = 1/(1 - t/rho) has c_k = rho^-k, so every
+    ratio c_{k}/c_{k+1} is rho; exp(alpha t) has c_{D-1}/c_D = D/alpha exactly;
+    a polynomial of degree < D has c_D = 0 (no finite singularity)."""
+    for rho in (Fraction(3, 2), Fraction(-5, 7), Fraction(1, 2)):
+        ser = [rho ** -k for k in range(10)]
+        assert O.fabry_ratio(ser, FX) == rho
+    alpha = Fraction(7, 8)
+    D = 9
+    ser = [alpha ** k / math.factorial(k) for k in range(D + 1)]
+    assert O.fabry_ratio(ser, FX) == Fraction(D) / alpha
+    assert O.fabry_ratio([Fraction(1), Fraction(2), Fraction(1), Fraction(0)], FX) is None
+
+
+def test_fabry_ratio_tends_to_nearest_singularity():
+    """Theorem 1's limit: for 1/((1 - t/rho)(1 - t/sigma)), |rho| < |sigma|,
+    the ratio tends to the nearer singular point rho as the order grows."""
+    rho, sigma = Fraction(1, 2), Fraction(3, 2)
+    a = [rho ** -k for k in range(40)]
+    b = [sigma ** -k for k in range(40)]
+    errs = []
+    for d in (8, 16, 32):
+        ser = O.conv(a, b, d, FX)
+        errs.append(abs(O.fabry_ratio(ser, FX) - rho))
+    assert errs[0] > errs[1] > errs[2] and errs[2] < Fraction(1, 10 ** 5)
+
+
+def test_sampled_residual_norm():
+    """the residual of the selected equations; all equations give
+    the full norm, a subset never exceeds it (sums of absolute values)."""
+    r = [[Fraction(i - k, 3) for i in range(5)] for k in range(4)]
+    assert O.residual_norm_sampled(r, range(5)) == O.series_norm(r)
+    assert O.residual_norm_sampled(r, [1, 3]) == max(abs(Fraction(1 - k, 3)) + abs(Fraction(3 - k, 3)) for k in range(4))
+    assert O.residual_norm_sampled(r, [2]) <= O.series_norm(r)
