@@ -243,8 +243,9 @@ int32_t ns_get_trace(ns_system* sys, int64_t* host, int32_t capacity_jobs, int32
 int32_t ns_get_qr_trace(ns_system* sys, int64_t* host, int32_t capacity_steps);
 /* Stage-chain trace of the last split stage loop (handle created with env
  * NS_STAGE_TRACE=1): per stage k, 4 globaltimer stamps (ns) of the critical
- * chain: start, pending rhs complete, b'_k written, dx_k written.  Returns d,
- * or -1 without a trace. */
+ * chain: start, pending rhs complete, b'_k written, dx_k written; then [d]
+ * stamps of the bulk: the last row of pend_k complete.  host_out holds 5 d
+ * values.  Returns d, or -1 without a trace. */
 int32_t ns_get_stage_trace(ns_system* sys, int64_t* host_out);
 /* Synchronises; per-class milliseconds accumulated over steps run with NS_LEDGER. */
 ns_status ns_get_ledger(ns_system* sys, ns_ledger* host_out);

@@ -339,11 +339,12 @@ class NewtonSystem:
         return t[:nj], jb[:nj]
 
     def stage_trace(self):
-        """Critical-chain stamps of the last split stage loop (env NS_STAGE_TRACE=1 at create): [d][4] ns."""
-        t = np.zeros((self.d, 4), np.int64)
+        """Stamps of the last split stage loop (env NS_STAGE_TRACE=1 at create): critical chain
+        [d][4] ns, bulk pend_k completion [d] ns."""
+        t = np.zeros(5 * self.d, np.int64)
         if int(lib().ns_get_stage_trace(self._h, t.ctypes.data)) < 0:
             raise RuntimeError("no stage trace (create the handle with NS_STAGE_TRACE=1)")
-        return t
+        return t[:4 * self.d].reshape(self.d, 4), t[4 * self.d:]
 
     def last_launch_count(self) -> int:
         return int(lib().ns_last_launch_count(self._h))

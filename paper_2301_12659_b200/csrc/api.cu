@@ -113,7 +113,7 @@ void free_all(ns_system* s) {
                   s->coeff, s->rhs, s->b, s->A, s->A0, s->W, s->vhead, s->beta, s->rdiag, s->R, s->Qt,
                   s->invR, s->bp, s->dx, s->y, s->part, s->Minv, s->Z, s->pend, s->sflags, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
                   s->bar, s->status, s->bws, s->A0q, s->qr_flags, s->jobs, s->ser_off, s->pool, s->prog, s->left,
-                  s->left_init, s->trace, s->strace, s->sample_rows};
+                  s->left_init, s->trace, s->strace, s->sample_rows, s->bpart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& row : s->ev)
@@ -298,6 +298,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->y, (size_t)K * n) == cudaSuccess;
   ok &= dalloc(&s->Minv, (size_t)K * nn) == cudaSuccess;
   ok &= dalloc(&s->pend, (size_t)K * d * n) == cudaSuccess;
+  ok &= dalloc(&s->bpart, (size_t)std::max(1, d - 2) * n * K * 32) == cudaSuccess;  // bulk lane partials
   ok &= dalloc(&s->sflags, 2 * d + 2) == cudaSuccess;
   ok &= dalloc(&s->Z, (size_t)K * nn) == cudaSuccess;
   {
@@ -327,7 +328,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->left, M) == cudaSuccess;
   ok &= dalloc(&s->left_init, M) == cudaSuccess;
   if (const char* e = getenv("NS_STAGE_TRACE"))
-    if (atoi(e)) ok &= dalloc(&s->strace, (size_t)4 * s->d) == cudaSuccess;
+    if (atoi(e)) ok &= dalloc(&s->strace, (size_t)5 * s->d) == cudaSuccess;
   if (const char* e = getenv("NS_TRACE"))
     if (atoi(e)) ok &= dalloc(&s->trace, 3 * jobs.size() + 6 * 256) == cudaSuccess;
   if (!ok) return fail(NS_ENOMEM);
@@ -440,7 +441,7 @@ int32_t ns_get_qr_trace(ns_system* s, int64_t* host, int32_t capacity_steps) {
 int32_t ns_get_stage_trace(ns_system* s, int64_t* host) {
   if (!s || !s->strace || !host) return -1;
   if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-  if (cudaMemcpy(host, s->strace, sizeof(long long) * 4 * s->d, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  if (cudaMemcpy(host, s->strace, sizeof(long long) * 5 * s->d, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
   return s->d;
 }
 

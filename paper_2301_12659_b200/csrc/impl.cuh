@@ -121,7 +121,7 @@ ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
     CK(cudaMemsetAsync(s->sflags, 0, sizeof(int) * (2 * s->d + 2), st));
     DevSys ds = devsys(s);
     ns::Stage2Args a{s->b, s->A, s->Minv, s->bp, s->dx, s->pend, s->sflags, s->sflags + s->d,
-                     (unsigned*)(s->sflags + 2 * s->d), Q, k_lo, s->strace};  // sflags[0]: dx published counter
+                     (unsigned*)(s->sflags + 2 * s->d), Q, k_lo, s->strace, s->bpart};  // sflags[0]: dx published counter
     unsigned* bar = s->bar + 2;
     void* args[] = {&ds, &a, &bar};
     CK(cudaLaunchCooperativeKernel((const void*)ns::stage2_kernel<K>, dim3(s->grid_st2), dim3(s->st2_threads), args,

@@ -368,9 +368,13 @@ __global__ void __launch_bounds__(256) invert_tiles_kernel(int n, int TB, const 
 
 // M = R^{-1} Q^T (row-major [K][n][n]) by tiled back substitution on the n
 // columns of Q^T, tiles last to first:  Z_t = Q^T_t - sum_{c >= t1} R[t][c] M[c],
-// M_t = invR_t Z_t.  One lane per column j, serial over c (once per QR).
+// M_t = invR_t Z_t.  Each output entry (r, j) is a dot shared by a group of
+// FM_G lanes (lane s of the group sums c = c0 + s, c0 + s + FM_G, ... in
+// order, then a fixed butterfly): one lane per entry left every warp with a
+// serial chain of up to n 8d multiply-adds (issue bound, 0.92 ms at C3).
 // With M each stage's "Q^T b then back substitution" is one matvec
 // dx_k = M b'_k (same algebra, R^{-1}(Q^T b) = (R^{-1} Q^T) b).
+constexpr int FM_G = 4;
 template <int K>
 __global__ void __launch_bounds__(128) form_m_kernel(int n, int TB, const double* __restrict__ R,
                                                      const double* __restrict__ Qt, const double* __restrict__ invR,
@@ -379,29 +383,36 @@ __global__ void __launch_bounds__(128) form_m_kernel(int n, int TB, const double
   const int gw = gwarp(), nw = nwarps(), lane = lane_id();
   const int T = (n + TB - 1) / TB;
   const long long lsM = (long long)n * n, lsI = (long long)T * TB * TB;
-  const int jg = (n + 31) / 32;  // 32-column groups
+  constexpr int OPW = 32 / FM_G;  // outputs per warp task
+  const int sub = lane % FM_G;
   for (int t = T - 1; t >= 0; --t) {
     const int t0 = t * TB, t1 = min(n, t0 + TB);
-    for (int w = gw; w < (t1 - t0) * jg; w += nw) {
-      const int r = t0 + w / jg, j = (w % jg) * 32 + lane;
-      if (j < n) {
-        const md::mdv<K> acc = md::dot_ilp<K, (K == 8 ? 4 : 1)>(t1, n, 1, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
-          xa = md::load<K>(R, lsM, (long long)r * n + c);
-          yb = md::load_cg<K>(M, lsM, (long long)c * n + j);
-        });
+    const int nout = (t1 - t0) * n;
+    const int tasks = (nout + OPW - 1) / OPW;
+    for (int w = gw; w < tasks; w += nw) {
+      const int o = w * OPW + lane / FM_G;
+      const bool ok = o < nout;
+      const int r = ok ? t0 + o / n : t0, j = ok ? o % n : 0;
+      md::mdv<K> acc = md::zero<K>();
+      if (ok)
+        for (int c = t1 + sub; c < n; c += FM_G)
+          acc = md::fma_acc<K>(acc, md::load<K>(R, lsM, (long long)r * n + c), md::load_cg<K>(M, lsM, (long long)c * n + j));
+      acc = md::group_sum<K>(acc, FM_G);
+      if (ok && sub == 0)
         md::store_cg<K>(Z, lsM, (long long)r * n + j, md::sub<K>(md::load<K>(Qt, lsM, (long long)r * n + j), acc));
-      }
     }
     gb.sync();
-    for (int w = gw; w < (t1 - t0) * jg; w += nw) {
-      const int r = t0 + w / jg, j = (w % jg) * 32 + lane;
-      if (j < n) {
-        const md::mdv<K> acc = md::dot_ilp<K, (K == 8 ? 4 : 1)>(t0, t1, 1, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
-          xa = md::load<K>(invR, lsI, (long long)t * TB * TB + (long long)(r - t0) * TB + (c - t0));
-          yb = md::load_cg<K>(Z, lsM, (long long)c * n + j);
-        });
-        md::store_cg<K>(M, lsM, (long long)r * n + j, acc);
-      }
+    for (int w = gw; w < tasks; w += nw) {
+      const int o = w * OPW + lane / FM_G;
+      const bool ok = o < nout;
+      const int r = ok ? t0 + o / n : t0, j = ok ? o % n : 0;
+      md::mdv<K> acc = md::zero<K>();
+      if (ok)
+        for (int c = t0 + sub; c < t1; c += FM_G)
+          acc = md::fma_acc<K>(acc, md::load<K>(invR, lsI, (long long)t * TB * TB + (long long)(r - t0) * TB + (c - t0)),
+                               md::load_cg<K>(Z, lsM, (long long)c * n + j));
+      acc = md::group_sum<K>(acc, FM_G);
+      if (ok && sub == 0) md::store_cg<K>(M, lsM, (long long)r * n + j, acc);
     }
     gb.sync();
   }
@@ -555,7 +566,10 @@ __global__ void __launch_bounds__(256) stage_kernel(DevSys s, StageArgs a, unsig
 // Each (k', row) pair is owned by one bulk warp (lane-held, up to 32 per
 // group) that applies k = k_lo, k_lo+1, ... in order, so
 // pend_{k'} = b_{k'} - sum_{j >= 2} A_j dx_{k'-j} accumulates in a fixed order
-// (deterministic) whatever the timing; among its pairs with work available
+// (deterministic) whatever the timing: lane l of the pair's warp keeps its
+// partial sum over the row entries e = l (mod 32) for k = k_lo, k_lo+1, ...
+// in a per-pair slot (part), and the warp butterfly runs once, after the
+// last k (one md reduction per pair instead of one per (pair, k)); among its pairs with work available
 // the warp always takes the most urgent (smallest k').  (Moving the j = 2
 // term into the critical chain too was measured slower: the chain's row dots
 // are FP64-issue bound, NS_STAGE_TRACE.)
@@ -573,6 +587,7 @@ struct Stage2Args {
   int Q;               // CTAs in the critical group
   int k_lo;            // first active stage (stages below: dx = 0, reading R34); last = s.dc - 1
   long long* tr;       // [d][4] globaltimer stamps of the critical chain (NS_STAGE_TRACE), or nullptr
+  double* part;        // [npairs][K][32] per-lane partial sums of the bulk pairs
 };
 
 __device__ __forceinline__ void sub_sync(unsigned* cnt, unsigned& target, unsigned nq) {
@@ -706,19 +721,34 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
     }
   } else {
     // ---------------- bulk group: (k', i) pairs, k' = k_lo+2..dc-1; a warp holds up to 32
-    // pairs (one per lane, ascending k') and always serves the most urgent one with work
+    // pairs (one per lane, ascending k') and always serves the most urgent one with work.
+    // Work unit = one 32-entry chunk of row i for one k (one fused multiply-add per lane),
+    // so a newly urgent pair waits for at most one chunk, not a whole row dot.  Units of a
+    // pair run in the order (k ascending, chunk ascending); the lane partials stay in
+    // registers while the warp keeps serving the same pair and go to the pair's slot
+    // (part) when it switches.
     const int bw = (blockIdx.x - a.Q) * wpb + wib, nbw = ((int)gridDim.x - a.Q) * wpb;
     const int npairs = (dc - 2 - k_lo) * n;
+    const long long lsA = (long long)d * s.nnz;
     int avail = 0;  // dx published so far (this warp's view)
     for (int g0 = bw; g0 < npairs; g0 += 32 * nbw) {
       const int p = g0 + lane * nbw;
       const bool has = p < npairs;
       const int kp = has ? k_lo + 2 + p / n : 0, i = has ? p % n : 0;
-      int pk = k_lo;  // next dx_k to apply to pend_{kp} row i; complete after k = kp - 2
-      bool live = has;
+      const int len = has ? s.row_ptr[i + 1] - s.row_ptr[i] : 0;
+      const int nch = max(1, (len + 31) / 32);
+      const int units = has ? (kp - 1 - k_lo) * nch : 0;  // k = k_lo..kp-2, nch chunks each
+      int pu = 0;                                          // units done
+      bool live = units > 0;
+      int cur = -1;  // pair whose lane partials are in acc (warp-uniform)
+      md::mdv<K> acc = md::zero<K>();
       for (;;) {
         if (!__any_sync(0xffffffffu, live)) break;
-        const unsigned m = __ballot_sync(0xffffffffu, live && pk < avail);
+        // refresh the published count every round (a stale count would hide a
+        // newly urgent pair behind the backlog of less urgent work)
+        if (lane == 0 && ld_relaxed_s32(a.ndx) > avail) avail = ld_acquire(a.ndx);
+        avail = __shfl_sync(0xffffffffu, avail, 0);
+        const unsigned m = __ballot_sync(0xffffffffu, live && k_lo + pu / nch < avail);
         if (m == 0) {  // nothing available: wait for the next dx
           if (lane == 0) {
             while (ld_relaxed_s32(a.ndx) <= avail) {
@@ -730,17 +760,47 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
         }
         const int src = __ffs(m) - 1;
         const int skp = __shfl_sync(0xffffffffu, kp, src), si = __shfl_sync(0xffffffffu, i, src);
-        const int spk = __shfl_sync(0xffffffffu, pk, src);
-        const md::mdv<K> dot = row_dot_A<K>(s, a.A, skp - spk, a.dx + (long long)spk * n, lsV, si);
-        if (lane == 0) {
-          const long long e = (long long)skp * n;
-          md::store_cg<K>(a.pend + e, lsV, si, md::sub<K>(md::load_cg<K>(a.pend + e, lsV, si), dot));
-          if (spk == skp - 2)  // last contribution to pend_{k'} row i
-            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.pdone + skp) : "memory");
+        const int spu = __shfl_sync(0xffffffffu, pu, src), sp = __shfl_sync(0xffffffffu, p, src);
+        const int snch = __shfl_sync(0xffffffffu, nch, src), sunits = __shfl_sync(0xffffffffu, units, src);
+        const int sk = k_lo + spu / snch, sch = spu % snch;
+        if (sp != cur) {  // switch pairs: park the current partials, fetch the new ones
+          if (cur >= 0) {
+            double* slot = a.part + (long long)cur * K * 32 + lane;
+#pragma unroll
+            for (int l = 0; l < K; ++l) slot[32 * l] = acc.x[l];
+          }
+          if (spu == 0) {
+            acc = md::zero<K>();
+          } else {
+            const double* slot = a.part + (long long)sp * K * 32 + lane;
+#pragma unroll
+            for (int l = 0; l < K; ++l) acc.x[l] = slot[32 * l];
+          }
+          cur = sp;
+        }
+        {
+          const int e = s.row_ptr[si] + sch * 32 + lane;
+          if (e < s.row_ptr[si + 1])
+            acc = md::fma_acc<K>(acc, md::load<K>(a.A + (long long)(skp - sk) * s.nnz, lsA, e),
+                                 md::load_cg<K>(a.dx + (long long)sk * n, lsV, s.col_idx[e]));
+        }
+        if (spu == sunits - 1) {  // last unit of pend_{k'} row i: reduce the lanes once
+          const md::mdv<K> tot = md::group_sum<K>(acc, 32);
+          if (lane == 0) {
+            const long long e = (long long)skp * n;
+            md::store_cg<K>(a.pend + e, lsV, si, md::sub<K>(md::load_cg<K>(a.pend + e, lsV, si), tot));
+            if (a.tr) {  // trace: when the last row of pend_{k'} completes, and the unit count
+              __threadfence();
+              if (atomicAdd(a.pdone + skp, 1) == n - 1) a.tr[4 * d + skp] = gtimer();
+            } else {
+              asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.pdone + skp) : "memory");
+            }
+          }
+          cur = -1;
         }
         if (lane == src) {
-          ++pk;
-          live = pk <= kp - 2;
+          ++pu;
+          live = pu < units;
         }
       }
     }

@@ -56,6 +56,7 @@ struct ns_system {
   int conv_mode = 0;           // eval/diff conv mode bits (NS_CONV_MODE, evaldiff.cuh)
   bool stage_split = true;     // critical group + right-looking bulk updates (stage2_kernel)
   double* pend = nullptr;      // [K][d][n] pending right-hand sides (stage2)
+  double* bpart = nullptr;     // [(d-2) n][K][32] per-lane partial sums of the bulk updates (stage2)
   int* sflags = nullptr;       // [2d + 2] dx published, pend rows done, critical barrier  // dynamic smem requested by the QR kernel to own its SMs
   size_t ed_smem = 0;
   bool qr_cached = false;

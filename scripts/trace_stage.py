@@ -19,11 +19,16 @@ for _ in range(3):
     xx = x.clone()
     h.step(xx)
 torch.cuda.synchronize()
-t = h.stage_trace().astype(float)
+t, pd = h.stage_trace()
+t = t.astype(float)
+pd = pd.astype(float)
+# bulk latency: dx_{k-2} published (t[k-2, 3]) -> last row of pend_k (pd[k])
+lat = [(pd[k] - t[k - 2, 3]) / 1e3 for k in range(2, len(pd)) if pd[k] > 0]
 d = np.diff(t, axis=1) / 1e3
 per = np.diff(t[:, 0]) / 1e3
 out = {"config": cfg, "us_mean": {"wait_pend": float(d[:, 0].mean()), "rowdot_b'": float(d[:, 1].mean()),
                                   "matvec_dx": float(d[:, 2].mean())},
        "stage_period_us": float(per.mean()), "span_us": float((t[-1, 3] - t[0, 0]) / 1e3),
+       "bulk_latency_us": [round(v, 2) for v in lat],
        "per_stage_us": [[round(v, 2) for v in row] for row in d.tolist()]}
 print(json.dumps(out))
