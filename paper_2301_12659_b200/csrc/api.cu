@@ -298,7 +298,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->y, (size_t)K * n) == cudaSuccess;
   ok &= dalloc(&s->Minv, (size_t)K * nn) == cudaSuccess;
   ok &= dalloc(&s->pend, (size_t)K * d * n) == cudaSuccess;
-  ok &= dalloc(&s->bpart, (size_t)std::max(1, d - 2) * n * K * 32) == cudaSuccess;  // bulk lane partials
+  ok &= dalloc(&s->bpart, (size_t)std::max<long long>(1, (long long)d - 2) * n * K * 32) == cudaSuccess;  // bulk lane partials
   ok &= dalloc(&s->sflags, 2 * d + 2) == cudaSuccess;
   ok &= dalloc(&s->Z, (size_t)K * nn) == cudaSuccess;
   {

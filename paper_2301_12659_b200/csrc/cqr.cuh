@@ -161,6 +161,10 @@ __global__ void __launch_bounds__(K == 8 ? 256 : 512) cluster_qr_kernel(DevSys s
                  fullC0 = cq::smem_u32(bars + 3 * RS);
   const unsigned vt0 = cq::smem_u32(vt), sc0 = cq::smem_u32(sc);
   auto col_ptr = [&](int lc) { return cols + (size_t)lc * K * n; };
+  // phase stamps (trace only) in the unused look-ahead row n-1: start, columns
+  // loaded, steps done, R/Q^T written, M written
+  long long* ph_tr = (tr && rank == 0 && threadIdx.x == 0) ? tr + 8LL * (n - 1) : nullptr;
+  if (ph_tr) ph_tr[0] = gtimer();
 
   // ---- A_0 (formed from x by warp per equation into W, or read from A0) and I
   if (x) {
@@ -203,6 +207,7 @@ __global__ void __launch_bounds__(K == 8 ? 256 : 512) cluster_qr_kernel(DevSys s
     }
   }
   __syncthreads();
+  if (ph_tr) ph_tr[1] = gtimer();
 
   // ---- publishing helpers (called by the whole owner warp)
   // A part of reflector jj: the whole column (rows > jj are v; consumers read
@@ -346,6 +351,7 @@ __global__ void __launch_bounds__(K == 8 ? 256 : 512) cluster_qr_kernel(DevSys s
     for (int p = lane; p < P; p += 32) cq::arrive_remote(cq::mapa(empty0 + 8 * s, p));
   }
   __syncthreads();
+  if (ph_tr) ph_tr[2] = gtimer();
 
   // ---- output: R (row-major upper, diagonal alpha), Q^T (row-major)
   for (int e = threadIdx.x; e < CPC * n; e += blockDim.x) {
@@ -359,6 +365,7 @@ __global__ void __launch_bounds__(K == 8 ? 256 : 512) cluster_qr_kernel(DevSys s
       else if (c < ncol) Qt[((size_t)l * n + r) * n + (c - n)] = v;
     }
   }
+  if (ph_tr) ph_tr[3] = gtimer();
   if (sh.withM && Mout) {
     // R columns (rows <= c final, R_cc = alpha_c) into every CTA's Rs
     cq::fence_proxy_async();
@@ -423,6 +430,7 @@ __global__ void __launch_bounds__(K == 8 ? 256 : 512) cluster_qr_kernel(DevSys s
       }
     }
   }
+  if (ph_tr) ph_tr[4] = gtimer();
   cq::cluster_sync_all();  // no CTA leaves while DSMEM traffic to it may be in flight
 }
 

@@ -103,7 +103,9 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
     double *M = s->Minv, *Z = s->Z;
     unsigned* bar2 = s->bar + 4;
     void* margs[] = {&n, &TB, (void*)&R, (void*)&Qt, (void*)&iR, &M, &Z, &bar2};
-    CK(cudaLaunchCooperativeKernel((const void*)ns::form_m_kernel<K>, dim3(s->grid_st), dim3(128), margs, 0, st));
+    // 8 warps per SM: the md chains are dependent DADD sequences, one warp per
+    // SMSP left the FP64 pipe 90% idle (ncu, C3)
+    CK(cudaLaunchCooperativeKernel((const void*)ns::form_m_kernel<K>, dim3(s->grid_st), dim3(256), margs, 0, st));
     s->last_launches += 1;
   }
   CK(cudaGetLastError());
@@ -171,7 +173,10 @@ ns_status setup_grids(ns_system* s) {
   // CTAs than SMs (a grid barrier costs more with every CTA); env overrides for tuning
   // one warp per column of [A0 | I] while that fits in one CTA per SM of 4 warps;
   // larger systems use 8 warps per CTA (the column updates are throughput work)
-  s->qr_threads = (2 * s->n > 4 * s->sms) ? 256 : 128;
+  // 8 warps per CTA: the grid QR then holds half as many SMs (reserved, below),
+  // leaving them to the concurrent eval/diff (C3: 10.25 vs 10.99 ms per step)
+  s->qr_threads = 256;
+  if (const char* e = getenv("NS_QR_THREADS")) s->qr_threads = atoi(e) >= 256 ? 256 : 128;
   s->grid_qr = std::min(s->sms, std::max(1, (2 * s->n + s->qr_threads / 32 - 1) / (s->qr_threads / 32)));
   // The QR is latency-bound and runs concurrently with eval/diff; a large
   // dynamic shared-memory request keeps eval/diff CTAs off the QR's SMs

@@ -374,9 +374,9 @@ __global__ void __launch_bounds__(256) invert_tiles_kernel(int n, int TB, const 
 // serial chain of up to n 8d multiply-adds (issue bound, 0.92 ms at C3).
 // With M each stage's "Q^T b then back substitution" is one matvec
 // dx_k = M b'_k (same algebra, R^{-1}(Q^T b) = (R^{-1} Q^T) b).
-constexpr int FM_G = 4;
+constexpr int FM_G = 8;
 template <int K>
-__global__ void __launch_bounds__(128) form_m_kernel(int n, int TB, const double* __restrict__ R,
+__global__ void __launch_bounds__(256) form_m_kernel(int n, int TB, const double* __restrict__ R,
                                                      const double* __restrict__ Qt, const double* __restrict__ invR,
                                                      double* M, double* Z, unsigned* bar) {
   GridBarrier gb(bar, 0u);
