@@ -242,7 +242,18 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
       dot = md::fma_acc<K>(dot, v0, wj);
       const md::mdv<K> nw_ = md::neg<K>(md::mul<K>(bt, dot));
       const bool look = (c == j + 1 && c < n);
-      md::mdv<K> sig = md::zero<K>(), x0 = md::zero<K>();
+      // look-ahead norm as unnormalised level sums (no renormalisation per term),
+      // one lazy-level butterfly (as in cqr.cuh): a shorter chain to reflector j+1
+      double sg[K];
+#pragma unroll
+      for (int l = 0; l < K; ++l) sg[l] = 0.0;
+      md::mdv<K> x0 = md::zero<K>();
+      auto sg_add = [&](const md::mdv<K>& w) {
+        double pl[K];
+        md::prod_levels<K>(w, w, pl);
+#pragma unroll
+        for (int l = 0; l < K; ++l) md::level_insert<K>(sg, l, pl[l]);
+      };
       if (first) {
 #pragma unroll
         for (int q = 0; q < S; ++q) {
@@ -251,7 +262,7 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
             const md::mdv<K> v = (r == j) ? v0 : vr[q];
             const md::mdv<K> w = md::fma_acc<K>(wr[q], nw_, v);
             md::store_cg<K>(W, ls, (long long)c * n + r, w);
-            if (look && r > j) sig = md::fma_acc<K>(sig, w, w);  // look-ahead norm, same pass
+            if (look && r > j) sg_add(w);  // look-ahead norm, same pass
             if (r == j + 1) x0 = w;
           }
         }
@@ -259,7 +270,7 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
           const md::mdv<K> w =
               md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)c * n + r), nw_, md::load_cg<K>(W, ls, (long long)j * n + r));
           md::store_cg<K>(W, ls, (long long)c * n + r, w);
-          if (look) sig = md::fma_acc<K>(sig, w, w);
+          if (look) sg_add(w);
         }
       } else {
         for (int r = j + lane; r < n; r += 32) {
@@ -271,7 +282,7 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
       if (look) {
         __syncwarp();
         if (lane == 0) flag_set(fA + j + 1, epoch);  // column j+1 final below its diagonal
-        sig = md::group_sum<K>(sig, 32);
+        const md::mdv<K> sig = md::group_sum_levels<K>(sg, 32);
         x0 = md::shfl<K>(x0, 1);  // row j+1 lives in lane 1
         reflector_from_sigma<K>(n, j + 1, sig, x0, W, vhead, beta, rdiag, status);
         __syncwarp();
