@@ -200,24 +200,34 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
     }
     constexpr int MAXC = 4;  // partial dots kept in flight per warp (more columns: dot recomputed)
     md::mdv<K> part[MAXC];
+    // partial dots as unnormalised level sums, one lazy-level butterfly each
+    auto lv_add = [&](double (&sl)[K], const md::mdv<K>& a, const md::mdv<K>& b) {
+      double pl[K];
+      md::prod_levels<K>(a, b, pl);
+#pragma unroll
+      for (int l = 0; l < K; ++l) md::level_insert<K>(sl, l, pl[l]);
+    };
     {
-      md::mdv<K> p = md::zero<K>();
+      double sl[K];
+#pragma unroll
+      for (int l = 0; l < K; ++l) sl[l] = 0.0;
 #pragma unroll
       for (int q = 0; q < S; ++q) {
         const int r = j + lane + 32 * q;
-        if (r > j && r < n) p = md::fma_acc<K>(p, vr[q], wr[q]);
+        if (r > j && r < n) lv_add(sl, vr[q], wr[q]);
       }
       for (int r = j + lane + 32 * S; r < n; r += 32)
-        p = md::fma_acc<K>(p, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)c0 * n + r));
-      part[0] = md::group_sum<K>(p, 32);
+        lv_add(sl, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)c0 * n + r));
+      part[0] = md::group_sum_levels<K>(sl, 32);
     }
     int nc = 1;
     for (int c = c0 + nw; c < ncol && nc < MAXC; c += nw, ++nc) {
-      const md::mdv<K> p = md::dot_ilp<K, 1>(j + 1 + lane, n, 32, [&](int r, md::mdv<K>& xa, md::mdv<K>& yb) {
-        xa = md::load_cg<K>(W, ls, (long long)j * n + r);
-        yb = md::load_cg<K>(W, ls, (long long)c * n + r);
-      });
-      part[nc] = md::group_sum<K>(p, 32);
+      double sl[K];
+#pragma unroll
+      for (int l = 0; l < K; ++l) sl[l] = 0.0;
+      for (int r = j + 1 + lane; r < n; r += 32)
+        lv_add(sl, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)c * n + r));
+      part[nc] = md::group_sum_levels<K>(sl, 32);
     }
     flag_wait(fB + j, epoch);
     __syncwarp();
