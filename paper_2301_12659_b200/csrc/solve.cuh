@@ -22,6 +22,25 @@ __device__ __forceinline__ int gwarp() { return (blockIdx.x * blockDim.x + threa
 __device__ __forceinline__ int nwarps() { return (gridDim.x * blockDim.x) >> 5; }
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// warp dot sum_t a_t b_t over t = t0, t0 + dt, ... < t1 (per lane), as
+// unnormalised level sums (md::prod_levels + level_insert: no renormalisation
+// per term) and one lazy-level butterfly over the warp
+template <int K, typename Term>
+__device__ __forceinline__ md::mdv<K> warp_dot_levels(int t0, int t1, int dt, Term term) {
+  double sl[K];
+#pragma unroll
+  for (int l = 0; l < K; ++l) sl[l] = 0.0;
+  for (int t = t0; t < t1; t += dt) {
+    md::mdv<K> a, b;
+    term(t, a, b);
+    double pl[K];
+    md::prod_levels<K>(a, b, pl);
+#pragma unroll
+    for (int l = 0; l < K; ++l) md::level_insert<K>(sl, l, pl[l]);
+  }
+  return md::group_sum_levels<K>(sl, 32);
+}
+
 // ------------------------------------------------------------------ QR
 // W: column-major work matrix, limb planes: W[(l*ncol + c)*n + r], ncol = 2n.
 template <int K, bool CG>
@@ -629,11 +648,10 @@ __device__ md::mdv<K> row_dot_A(const DevSys& s, const double* A, int j, const d
   const int lane = threadIdx.x & 31;
   const long long lsA = (long long)s.d * s.nnz;
   const int r0 = s.row_ptr[i], r1 = s.row_ptr[i + 1];
-  const md::mdv<K> acc = md::dot_ilp<K, 1>(r0 + lane, r1, 32, [&](int e, md::mdv<K>& xa, md::mdv<K>& yb) {
+  return warp_dot_levels<K>(r0 + lane, r1, 32, [&](int e, md::mdv<K>& xa, md::mdv<K>& yb) {
     xa = md::load<K>(A + (long long)j * s.nnz, lsA, e);
     yb = md::load_cg<K>(v, lsV, s.col_idx[e]);
   });
-  return md::group_sum<K>(acc, 32);
 }
 
 template <int K>
@@ -696,11 +714,18 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
           md::mdv<K> xv[RQ];
 #pragma unroll
           for (int q = 0; q < RQ; ++q) xv[q] = (lane + 32 * q < len) ? md::load_cg<K>(xp, lsV, colc[q]) : md::zero<K>();
-          md::mdv<K> p = md::zero<K>();
+          double sl[K];
+#pragma unroll
+          for (int l = 0; l < K; ++l) sl[l] = 0.0;
 #pragma unroll
           for (int q = 0; q < RQ; ++q)
-            if (lane + 32 * q < len) p = md::fma_acc<K>(p, a1c[q], xv[q]);
-          v = md::sub<K>(v, md::group_sum<K>(p, 32));
+            if (lane + 32 * q < len) {
+              double pl[K];
+              md::prod_levels<K>(a1c[q], xv[q], pl);
+#pragma unroll
+              for (int l = 0; l < K; ++l) md::level_insert<K>(sl, l, pl[l]);
+            }
+          v = md::sub<K>(v, md::group_sum_levels<K>(sl, 32));
         }
         if (lane == 0) md::store_cg<K>(a.bp + (long long)k * n, lsV, row, v);
         sub_sync(a.cbar, target, a.Q);
@@ -709,11 +734,18 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
         md::mdv<K> bv[RQ];
 #pragma unroll
         for (int q = 0; q < RQ; ++q) bv[q] = (lane + 32 * q < n) ? md::load_cg<K>(bk, lsV, lane + 32 * q) : md::zero<K>();
-        md::mdv<K> acc = md::zero<K>();
+        double sl[K];
+#pragma unroll
+        for (int l = 0; l < K; ++l) sl[l] = 0.0;
 #pragma unroll
         for (int q = 0; q < RQ; ++q)
-          if (lane + 32 * q < n) acc = md::fma_acc<K>(acc, mc[q], bv[q]);
-        acc = md::group_sum<K>(acc, 32);
+          if (lane + 32 * q < n) {
+            double pl[K];
+            md::prod_levels<K>(mc[q], bv[q], pl);
+#pragma unroll
+            for (int l = 0; l < K; ++l) md::level_insert<K>(sl, l, pl[l]);
+          }
+        const md::mdv<K> acc = md::group_sum_levels<K>(sl, 32);
         if (lane == 0) md::store_cg<K>(a.dx + (long long)k * n, lsV, row, acc);
         sub_sync(a.cbar, target, a.Q);
         if (trc) a.tr[4 * k + 3] = gtimer();
@@ -729,11 +761,10 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
       sub_sync(a.cbar, target, a.Q);
       if (trc) a.tr[4 * k + 2] = gtimer();
       for (int r = cw; r < n; r += ncw) {
-        md::mdv<K> acc = md::dot_ilp<K, 1>(lane, n, 32, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
+        const md::mdv<K> acc = warp_dot_levels<K>(lane, n, 32, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
           xa = md::load<K>(a.M, lsM, (long long)r * n + c);
           yb = md::load_cg<K>(a.bp + (long long)k * n, lsV, c);
         });
-        acc = md::group_sum<K>(acc, 32);
         if (lane == 0) md::store_cg<K>(a.dx + (long long)k * n, lsV, r, acc);
       }
       sub_sync(a.cbar, target, a.Q);
