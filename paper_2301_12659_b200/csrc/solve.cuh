@@ -832,12 +832,16 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
         }
         {
           const int e = s.row_ptr[si] + sch * 32 + lane;
-          if (e < s.row_ptr[si + 1])
-            acc = md::fma_acc<K>(acc, md::load<K>(a.A + (long long)(skp - sk) * s.nnz, lsA, e),
-                                 md::load_cg<K>(a.dx + (long long)sk * n, lsV, s.col_idx[e]));
+          if (e < s.row_ptr[si + 1]) {  // acc holds unnormalised level sums (no renormalisation per term)
+            double pl[K];
+            md::prod_levels<K>(md::load<K>(a.A + (long long)(skp - sk) * s.nnz, lsA, e),
+                               md::load_cg<K>(a.dx + (long long)sk * n, lsV, s.col_idx[e]), pl);
+#pragma unroll
+            for (int l = 0; l < K; ++l) md::level_insert<K>(acc.x, l, pl[l]);
+          }
         }
         if (spu == sunits - 1) {  // last unit of pend_{k'} row i: reduce the lanes once
-          const md::mdv<K> tot = md::group_sum<K>(acc, 32);
+          const md::mdv<K> tot = md::group_sum_levels<K>(acc.x, 32);
           if (lane == 0) {
             const long long e = (long long)skp * n;
             md::store_cg<K>(a.pend + e, lsV, si, md::sub<K>(md::load_cg<K>(a.pend + e, lsV, si), tot));
