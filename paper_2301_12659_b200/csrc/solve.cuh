@@ -433,11 +433,17 @@ __global__ void __launch_bounds__(256) form_m_kernel(int n, int TB, const double
       const int o = w * OPW + lane / FM_G;
       const bool ok = o < nout;
       const int r = ok ? t0 + o / n : t0, j = ok ? o % n : 0;
-      md::mdv<K> acc = md::zero<K>();
+      double sl[K];
+#pragma unroll
+      for (int l = 0; l < K; ++l) sl[l] = 0.0;
       if (ok)
-        for (int c = t1 + sub; c < n; c += FM_G)
-          acc = md::fma_acc<K>(acc, md::load<K>(R, lsM, (long long)r * n + c), md::load_cg<K>(M, lsM, (long long)c * n + j));
-      acc = md::group_sum<K>(acc, FM_G);
+        for (int c = t1 + sub; c < n; c += FM_G) {
+          double pl[K];
+          md::prod_levels<K>(md::load<K>(R, lsM, (long long)r * n + c), md::load_cg<K>(M, lsM, (long long)c * n + j), pl);
+#pragma unroll
+          for (int l = 0; l < K; ++l) md::level_insert<K>(sl, l, pl[l]);
+        }
+      const md::mdv<K> acc = md::group_sum_levels<K>(sl, FM_G);
       if (ok && sub == 0)
         md::store_cg<K>(Z, lsM, (long long)r * n + j, md::sub<K>(md::load<K>(Qt, lsM, (long long)r * n + j), acc));
     }
@@ -446,12 +452,18 @@ __global__ void __launch_bounds__(256) form_m_kernel(int n, int TB, const double
       const int o = w * OPW + lane / FM_G;
       const bool ok = o < nout;
       const int r = ok ? t0 + o / n : t0, j = ok ? o % n : 0;
-      md::mdv<K> acc = md::zero<K>();
+      double sl[K];
+#pragma unroll
+      for (int l = 0; l < K; ++l) sl[l] = 0.0;
       if (ok)
-        for (int c = t0 + sub; c < t1; c += FM_G)
-          acc = md::fma_acc<K>(acc, md::load<K>(invR, lsI, (long long)t * TB * TB + (long long)(r - t0) * TB + (c - t0)),
-                               md::load_cg<K>(Z, lsM, (long long)c * n + j));
-      acc = md::group_sum<K>(acc, FM_G);
+        for (int c = t0 + sub; c < t1; c += FM_G) {
+          double pl[K];
+          md::prod_levels<K>(md::load<K>(invR, lsI, (long long)t * TB * TB + (long long)(r - t0) * TB + (c - t0)),
+                             md::load_cg<K>(Z, lsM, (long long)c * n + j), pl);
+#pragma unroll
+          for (int l = 0; l < K; ++l) md::level_insert<K>(sl, l, pl[l]);
+        }
+      const md::mdv<K> acc = md::group_sum_levels<K>(sl, FM_G);
       if (ok && sub == 0) md::store_cg<K>(M, lsM, (long long)r * n + j, acc);
     }
     gb.sync();
@@ -879,14 +891,11 @@ __global__ void __launch_bounds__(256) residual_kernel(int n, int d, int dc, int
   for (long long row = gw; row < (long long)dc * nr; row += nw) {
     const int k = (int)(row / nr), i = rows ? rows[row % nr] : (int)(row % nr);
     md::mdv<K> acc = md::zero<K>();
-    if (k >= k_lo) {
-      for (int c = lane; c < n; c += 32) {
-        md::mdv<K> av = md::load<K>(A0, lsM, (long long)i * n + c);
-        md::mdv<K> xv = md::load<K>(dx + (long long)k * n, lsV, c);
-        acc = md::fma_acc<K>(acc, av, xv);
-      }
-      acc = md::group_sum<K>(acc, 32);
-    }
+    if (k >= k_lo)  // warp-uniform (row is per warp)
+      acc = warp_dot_levels<K>(lane, n, 32, [&](int c, md::mdv<K>& xa, md::mdv<K>& yb) {
+        xa = md::load<K>(A0, lsM, (long long)i * n + c);
+        yb = md::load<K>(dx + (long long)k * n, lsV, c);
+      });
     if (lane == 0) {
       md::mdv<K> r = (k >= k_lo) ? md::sub<K>(md::load<K>(bp + (long long)k * n, lsV, i), acc)
                                  : md::load<K>(b + (long long)k * n, lsV, i);
