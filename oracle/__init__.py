@@ -20,6 +20,10 @@ or in mpmath at at least twice the bits of the md precision under test:
 * ``newton.step``       x + dx and the norms ||b||, ||b - A dx||, ||dx||
 * ``newton.scales``     the running-error scales s_k of SURVEY.md 8(c) c.4 that
                         define the tolerance ||gpu_k - oracle_k|| <= tol_p s_k
+* ``newton.step_window`` one step on the stage window [k_lo, dc) (P:494-518, Eq.(11));
+                        ``newton.staggered_orders`` the Eq.(10) schedule (NEXT-1)
+* ``newton.fabry_ratio`` c_{D-1}/c_D (Theorem 1); ``newton.residual_norm_sampled``
+                        the residual of selected equations (NEXT-4)
 * ``paper``             values the paper prints (T1, T2, Eq.(13)-(16) counts)
 
 Parity status per function is listed in DESIGN.md "Oracle pins".  Entries
