@@ -82,7 +82,8 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
       CK(cudaLaunchKernelEx(&cfg, ns::cluster_qr_kernel<K, 4>, ds, xp, n, A0, W, R, Qt, rd, stt, sh, tr, Mo));
     s->last_launches += 1;
   } else {
-    void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch};
+    int ob = s->qr_owner_beta ? 1 : 0;
+    void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch, &ob};
     CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_kernel<K>, dim3(s->grid_qr), dim3(s->qr_threads),
                                    args, s->qr_smem_reserve, st));
     const long long tot = (long long)K * n * n;
@@ -177,6 +178,10 @@ ns_status setup_grids(ns_system* s) {
   // leaving them to the concurrent eval/diff (C3: 10.25 vs 10.99 ms per step)
   s->qr_threads = 256;
   if (const char* e = getenv("NS_QR_THREADS")) s->qr_threads = atoi(e) >= 256 ? 256 : 128;
+  // the owner forms beta once: at 8 warps per CTA the per-consumer reciprocals
+  // competed with the owner's chain for the FP64 pipes (C3 QR 7.03 -> 6.92 ms, C4 66.8 -> 63.4)
+  s->qr_owner_beta = true;
+  if (const char* e = getenv("NS_QR_OWNER_BETA")) s->qr_owner_beta = atoi(e) != 0;
   s->grid_qr = std::min(s->sms, std::max(1, (2 * s->n + s->qr_threads / 32 - 1) / (s->qr_threads / 32)));
   // The QR is latency-bound and runs concurrently with eval/diff; a large
   // dynamic shared-memory request keeps eval/diff CTAs off the QR's SMs

@@ -115,7 +115,8 @@ __device__ void apply_reflector(int n, int j, int c, double* W, const double* vh
 // and W[jj][jj] = alpha.
 template <int K>
 __device__ void reflector_from_sigma(int n, int jj, const md::mdv<K>& sig, const md::mdv<K>& x0, double* W,
-                                     double* vhead, double* beta, double* rdiag, unsigned* status) {
+                                     double* vhead, double* beta, double* rdiag, unsigned* status,
+                                     bool owner_beta = false) {
   const long long ls = 2LL * n * n;
   const int lane = lane_id();
   const md::mdv<K> nrm = md::sqrt<K>(sig);
@@ -123,7 +124,10 @@ __device__ void reflector_from_sigma(int n, int jj, const md::mdv<K>& sig, const
   const md::mdv<K> v0 = md::sub<K>(x0, alpha);
   // beta = -1/(alpha v0) is formed by the consumers; store alpha v0 (0 for a zero column)
   md::mdv<K> pav = md::zero<K>();
-  if (!md::is_zero<K>(sig)) pav = md::mul<K>(alpha, v0);
+  if (!md::is_zero<K>(sig)) {
+    pav = md::mul<K>(alpha, v0);
+    if (owner_beta) pav = md::neg<K>(md::recip<K>(pav));  // the slot holds beta itself
+  }
   else if (lane == 0 && status) atomicOr(status, ST_SINGULAR);
   if (lane == 0) {
     md::store_cg<K>(vhead, n, jj, v0);
@@ -158,7 +162,8 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
                                                              const double* __restrict__ A0,
                                                              double* W, double* vhead, double* beta,
                                                              double* rdiag, unsigned* bar,
-                                                             unsigned* status, int* flags, int epoch) {
+                                                             unsigned* status, int* flags, int epoch,
+                                                             int owner_beta) {
   const int ncol = 2 * n;
   const long long ls = (long long)ncol * n;
   const int gw = gwarp(), nw = nwarps(), lane = lane_id();
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
       sig = md::fma_acc<K>(sig, v, v);
     }
     sig = md::group_sum<K>(sig, 32);
-    reflector_from_sigma<K>(n, 0, sig, md::load_cg<K>(W, ls, 0), W, vhead, beta, rdiag, status);
+    reflector_from_sigma<K>(n, 0, sig, md::load_cg<K>(W, ls, 0), W, vhead, beta, rdiag, status, owner_beta != 0);
     __syncwarp();
     if (lane == 0) flag_set(flags + n, epoch);  // B[0]
   }
@@ -254,7 +259,9 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
     const md::mdv<K> pav = md::load_cg<K>(beta, n, j);  // alpha_j v0_j
     // beta_j = -1 / (alpha v0), formed here (each consumer) so that the owner's
     // critical chain ends at alpha v0; zero column -> beta = 0 (H = I)
-    const md::mdv<K> bt = md::is_zero<K>(pav) ? md::zero<K>() : md::neg<K>(md::recip<K>(pav));
+    // owner_beta: the owner formed beta once (one reciprocal per reflector instead of one
+    // per consumer warp competing for the FP64 pipes); else each consumer forms it
+    const md::mdv<K> bt = owner_beta ? pav : (md::is_zero<K>(pav) ? md::zero<K>() : md::neg<K>(md::recip<K>(pav)));
     int ic = 0;
     for (int c = c0; c < ncol; c += nw, ++ic) {
       md::mdv<K> dot;
@@ -313,7 +320,7 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
         if (lane == 0) flag_set(fA + j + 1, epoch);  // column j+1 final below its diagonal
         const md::mdv<K> sig = md::group_sum_levels<K>(sg, 32);
         x0 = md::shfl<K>(x0, 1);  // row j+1 lives in lane 1
-        reflector_from_sigma<K>(n, j + 1, sig, x0, W, vhead, beta, rdiag, status);
+        reflector_from_sigma<K>(n, j + 1, sig, x0, W, vhead, beta, rdiag, status, owner_beta != 0);
         __syncwarp();
         if (lane == 0) flag_set(fB + j + 1, epoch);
       }

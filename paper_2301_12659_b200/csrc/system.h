@@ -47,6 +47,7 @@ struct ns_system {
   int st_threads = 256;        // threads per CTA of the stage kernel
   int st2_threads = 64, grid_st2 = 0;  // split stage kernel (stage2_kernel): CTA size and grid
   int qr_threads = 128;        // threads per CTA of the QR kernel
+  bool qr_owner_beta = false;  // grid QR: the reflector's owner forms beta (NS_QR_OWNER_BETA)
   bool cqr_on = false;         // cluster QR (cqr.cuh) instead of householder_qr_kernel
   int cqr_P = 0, cqr_W = 0, cqr_CPC = 0, cqr_RS = 0, cqr_E = 0;
   size_t cqr_smem = 0;
