@@ -88,7 +88,7 @@ class System:
     eq_ptr: np.ndarray      # int32 [n+1]
     mono_ptr: np.ndarray    # int32 [M+1]
     var_idx: np.ndarray     # int32 [sum m]
-    coeff: np.ndarray       # float64 [K][M]  (md coefficients; here limb 0 only)
+    coeff: np.ndarray       # float64 [K][M]  md coefficients (limb planes)
     rhs: np.ndarray         # float64 [K][n][d]
     exact: tuple
     meta: dict = field(default_factory=dict)
@@ -108,8 +108,8 @@ class System:
         return [int(v) for v in self.var_idx[self.mono_ptr[t]:self.mono_ptr[t + 1]]]
 
     def coeff_fraction_pairs(self, t: int) -> tuple[int, int]:
-        # coefficients are single doubles (limb 0), reading R9
-        return frac_pair(float(self.coeff[0, t]))
+        # the exact value of the md coefficient: the sum of its limbs
+        return _sum_pairs(frac_pair(float(v)) for v in self.coeff[:, t])
 
 
 def _csr(eqs: list[list[list[int]]]):
@@ -163,7 +163,7 @@ def _rhs_exp(eqs, coeffs, alphas, n, d, K) -> np.ndarray:
         cs = []
         for vs in monos:
             Ss.append(_alpha_sum(alphas, vs))
-            cs.append(frac_pair(coeffs[t]))
+            cs.append(_cpair(coeffs[t]))
             t += 1
         for k in range(d):
             terms = []
@@ -183,7 +183,7 @@ def _rhs_inv1mt(eqs, coeffs, n, d, K) -> np.ndarray:
         for k in range(d):
             terms = []
             for j, vs in enumerate(monos):
-                cn, cd = frac_pair(coeffs[t + j])
+                cn, cd = _cpair(coeffs[t + j])
                 m = len(vs)
                 terms.append((cn * math.comb(k + m - 1, m - 1), cd))
             num, den = _sum_pairs(terms)
@@ -192,9 +192,17 @@ def _rhs_inv1mt(eqs, coeffs, n, d, K) -> np.ndarray:
     return rhs
 
 
+def _cpair(c) -> tuple[int, int]:
+    """a coefficient given as a float (exact dyadic) or as an exact (num, den) pair"""
+    return c if isinstance(c, tuple) else frac_pair(float(c))
+
+
 def _coeff_planes(coeffs, K):
+    """md coefficients [K][M], rounded limb by limb from their exact values."""
     c = np.zeros((K, len(coeffs)))
-    c[0, :] = coeffs
+    for t, v in enumerate(coeffs):
+        num, den = _cpair(v)
+        c[:, t] = rational_to_md(num, den, K)
     return c
 
 
@@ -215,23 +223,32 @@ def banded_two_column_system(n: int, w: int, D: int, K: int, seed: int = 0,
                              name: str = "TS3") -> System:
     """2-column format c1 x^E1 + c2 x^E2 = b(t) (Eq.(8)-(9)), banded
     (reading R9): E1 row i = {max(0,i-w+1)..i}; E2 row i = E1 row n-1-i;
-    c1 = 1, c2 ~ U[-1/2, 1/2]; exact solution exp(alpha_j t)."""
+    c1 = 1, c2 = RN_md(v/3) with v ~ U[-3/2, 3/2] (so c2 ~ U[-1/2, 1/2]); the factor
+    1/3 makes c2 a full md number (every limb nonzero; rounded limb by limb),
+    so the coefficient limbs 1..K-1 are exercised; the rhs is that of the
+    md-rounded c2, so exp(alpha_j t) is the exact solution (up to the rhs
+    rounding)."""
     E1 = [list(range(max(0, i - w + 1), i + 1)) for i in range(n)]
     E2 = [E1[n - 1 - i] for i in range(n)]
     eqs = [[E1[i], E2[i]] if E1[i] != E2[i] else [E1[i]] for i in range(n)]
     rng = np.random.Generator(np.random.PCG64(seed + 7919))
-    c2 = rng.uniform(-0.5, 0.5, size=n)
+    v = rng.uniform(-1.5, 1.5, size=n)
     coeffs = []
     for i in range(n):
         coeffs.append(1.0)
         if len(eqs[i]) == 2:
-            coeffs.append(float(c2[i]))
+            vn, vd = frac_pair(float(v[i]))
+            vn = vn - vn % 3 + 1  # numerator = 1 (mod 3): v/3 is not dyadic
+            coeffs.append((vn, 3 * vd))
     # monomials must appear in ascending variable-list order inside the CSR?  No:
     # the order inside an equation is the summation order (reading R20).
     alphas = draw_alphas(n, seed)
     eq_ptr, mono_ptr, var_idx = _csr(eqs)
-    rhs = _rhs_exp(eqs, coeffs, alphas, n, D + 1, K)
-    return System(name, n, D, K, eq_ptr, mono_ptr, var_idx, _coeff_planes(coeffs, K), rhs,
+    planes = _coeff_planes(coeffs, K)
+    # the rhs of the md-rounded coefficients (exp(alpha t) solves the system as stored)
+    exact_c = [_sum_pairs(frac_pair(float(l)) for l in planes[:, t]) for t in range(len(coeffs))]
+    rhs = _rhs_exp(eqs, exact_c, alphas, n, D + 1, K)
+    return System(name, n, D, K, eq_ptr, mono_ptr, var_idx, planes, rhs,
                   ("exp", alphas), {"seed": seed, "w": w})
 
 

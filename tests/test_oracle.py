@@ -447,3 +447,134 @@ def test_sampled_residual_norm():
     assert O.residual_norm_sampled(r, range(5)) == O.series_norm(r)
     assert O.residual_norm_sampled(r, [1, 3]) == max(abs(Fraction(1 - k, 3)) + abs(Fraction(3 - k, 3)) for k in range(4))
     assert O.residual_norm_sampled(r, [2]) <= O.series_norm(r)
+
+
+# ---------------------------------------------------------------- coefficients c != 1
+def _exact_exp_x(sys_):
+    """x_j = exp(alpha_j t) as exact rationals (not md-rounded): alpha_j^k / k!."""
+    al = [Fraction(a) for a in sys_.exact[1]]
+    return [[al[j] ** k / math.factorial(k) for k in range(sys_.d)] for j in range(sys_.n)]
+
+
+def test_two_column_jacobian_closed_form_negative_coefficients():
+    """2-column system c1 x^E1 + c2 x^E2 (Eq.(8)-(9)) with negative
+    md coefficients c2: at x_j = exp(alpha_j t) a monomial tau is exp(S_tau t)
+    and d/dx_j of it is exp((S_tau - alpha_j) t), so
+        A_k[i][j] = sum_{tau in eq i, tau ∋ j} c_tau (S_tau - alpha_j)^k / k!
+    (SURVEY c.5 closed form, summed with the signed coefficients), and
+    b_i = r_i - sum_tau c_tau S_tau^k/k! is the rounding of the stored rhs only.
+    A sign slip on c (abs(c), -c) or a dropped coefficient fails here."""
+    sys_ = synth.banded_two_column_system(7, 3, 5, 4, seed=3)
+    co = O.read_coeffs(sys_, FX)
+    assert any(c < 0 for c in co) and any(c.denominator % 3 == 0 or c.denominator > 2 ** 60 for c in co)
+    assert any(sys_.coeff[1:, t].any() for t in range(sys_.M))   # limbs 1..K-1 in use
+    xs = _exact_exp_x(sys_)
+    b, A = O.evaluate(sys_, xs, FX)
+    al = [Fraction(a) for a in sys_.exact[1]]
+    rhs = O.read_rhs(sys_, FX)
+    for i in range(sys_.n):
+        want = {}
+        val = [Fraction(0)] * sys_.d
+        for t in O.eq_monomials(sys_, i):
+            vs = O.monomial_vars(sys_, t)
+            S = sum(al[v] for v in vs)
+            for k in range(sys_.d):
+                val[k] += co[t] * S ** k / math.factorial(k)
+            for j in vs:
+                ser = want.setdefault(j, [Fraction(0)] * sys_.d)
+                for k in range(sys_.d):
+                    ser[k] += co[t] * (S - al[j]) ** k / math.factorial(k)
+        assert A[i] == want, i
+        for k in range(sys_.d):
+            assert b[i][k] == rhs[i][k] - val[k]
+            assert abs(b[i][k]) <= Fraction(2) ** -200 * (1 + abs(rhs[i][k]))
+
+
+def test_newton_two_column_negative_coefficients_converges():
+    """Quadratic convergence (SURVEY c.3) on the 2-column banded system with
+    signed md coefficients c2: from 'start' the iterated oracle steps reach
+    exp(alpha t) at coefficient k <= 2^i - 2 after i steps; a Jacobian with a
+    wrong coefficient sign (e.g. abs(c)) gives a chord iteration that does not.
+    From the exact solution the update is ~0 (fixed point)."""
+    F = O.MPField(600)
+    sys_ = synth.banded_two_column_system(6, 3, 6, 8, seed=11)
+    assert any(float(sys_.coeff[0, t]) < 0 for t in range(sys_.M))
+    n, d = sys_.n, sys_.d
+    ex = O.read_x(synth.make_x(sys_, "exact"), F)
+    xs = O.read_x(synth.make_x(sys_, "start", seed=5), F)
+    for it in range(1, 5):
+        b, A = O.evaluate(sys_, xs, F)
+        dx = O.solve(A, b, n, d, F)
+        xs = [[xs[j][k] + dx[k][j] for k in range(d)] for j in range(n)]
+        for k in range(min(2 ** it - 1, d)):
+            e = max(abs(xs[j][k] - ex[j][k]) for j in range(n))
+            assert e < F.num(2.0 ** -380), (it, k, e)
+    b, A = O.evaluate(sys_, ex, F)
+    dx = O.solve(A, b, n, d, F)
+    assert max(abs(v) for dk in dx for v in dk) < F.num(2.0 ** -400)
+
+
+# ---------------------------------------------------------------- tolerance scales (SURVEY c.4)
+def test_scales_hand_derived_inv1mt_and_negative_coefficient():
+    """s_b and s_A at x_j = 1/(1-t) (every coefficient 1): a product of m
+    variables has coefficients C(k+m-1, m-1), so for the triangular integer
+    system (eq i = x_0..x_i, rhs the same product)
+        s_b[k,i] = |r_i,k| + C(k+i, i) = 2 C(k+i, i),
+        s_A[(i,j)][k] = C(k+i-1, i-1) (i >= 1),  s_A[(0,0)] = (1, 0, 0, ...).
+    With a coefficient c = -1/2 on x_0 x_1 the scales carry |c| = 1/2."""
+    sys_ = synth.inv1mt_system(4, 6, 2)
+    x = synth.make_x(sys_, "exact")
+    sc = O.scales(sys_, x)
+    for i in range(4):
+        for k in range(7):
+            assert sc["s_b"][k, i] == 2 * math.comb(k + i, i)
+            for j in range(i + 1):
+                want = (1.0 if k == 0 else 0.0) if i == 0 else math.comb(k + i - 1, i - 1)
+                assert sc["s_A"][(i, j)][k] == want, (i, j, k)
+    sys2 = synth.custom_system([[[0]], [[0, 1]]], [1.0, -0.5], 5, 2, [1.0, 1.0])
+    x2 = np.zeros((2, 2, 6)); x2[0] = 1.0
+    sc2 = O.scales(sys2, x2)
+    for k in range(6):
+        assert sc2["s_b"][k, 1] == abs(sys2.rhs[0, 1, k]) + 0.5 * (k + 1)
+        assert sc2["s_A"][(1, 0)][k] == 0.5 and sc2["s_A"][(1, 1)][k] == 0.5
+
+
+def test_stage_scales_hand_derived_2x2():
+    """The running-error recursion of SURVEY c.4 worked by hand on the
+    integer system x_0 = r_0, x_0 x_1 = r_1 at x = 1/(1-t):
+    A_0 = [[1,0],[1,1]], |A_0^-1| = [[1,0],[1,1]], s_A_j = [[0,0],[1,1]] (j >= 1),
+    s_b_k = (2, 2(k+1)).  With dx = 0:  e = (2,4), (2,12), (2,28), s = 5, 13, 29.
+    With dx_0 = (1, 0):                 e = (3,6), (2,16), (2,36), s = 7, 17, 37."""
+    sys_ = synth.inv1mt_system(2, 2, 2)
+    x = synth.make_x(sys_, "exact")
+    sc = O.scales(sys_, x)
+    A0 = np.array([[1.0, 0.0], [1.0, 1.0]])
+    s, e = O.stage_scales(sys_, x, A0, np.zeros((3, 2)), sc["s_b"], sc["s_A"])
+    assert list(s) == [5, 13, 29] and e.tolist() == [[2, 4], [2, 12], [2, 28]]
+    dx = np.zeros((3, 2)); dx[0, 0] = 1.0
+    s, e = O.stage_scales(sys_, x, A0, dx, sc["s_b"], sc["s_A"])
+    assert list(s) == [7, 17, 37] and e.tolist() == [[3, 6], [2, 16], [2, 36]]
+
+
+# ---------------------------------------------------------------- QR reuse (x0_factor)
+def test_step_window_x0_factor():
+    """step_window(x0_factor=...) factors the A_0 of an earlier x_0 (the QR
+    "only once").  (1) With x0_factor = x it is the plain step, bit
+    for bit.  (2) With another x_0 the stage-0 solve uses that matrix, worked
+    by hand on x_0 = r_0, x_0 x_1 = r_1: A_0(x0f) = [[1,0],[x1f, x0f]], so
+    dx_0 = (b_0, (b_1 - x1f b_0) / x0f); later stages use the same factor."""
+    sys_ = synth.triangular_system(2, 3, 2, seed=4)
+    x = synth.make_x(sys_, "near", seed=6)
+    full = O.step_window(sys_, x, FX, 0, sys_.d)
+    same = O.step_window(sys_, x, FX, 0, sys_.d, x0_factor=x)
+    for key in ("dx", "x_new", "r"):
+        assert full[key] == same[key], key
+    xf = np.zeros((2, 2, 1)); xf[0, 0, 0] = 2.0; xf[0, 1, 0] = 3.0
+    mod = O.step_window(sys_, x, FX, 0, sys_.d, x0_factor=xf)
+    b = mod["b"]
+    assert mod["dx"][0][0] == b[0][0]
+    assert mod["dx"][0][1] == (b[1][0] - 3 * b[0][0]) / 2
+    # stage 1: A_0(x0f) dx_1 = b_1 - A_1 dx_0 with the true A_1
+    A1dx = O.matvec_sparse(mod["A"], 1, mod["dx"][0], 2, FX)
+    r0, r1 = b[0][1] - A1dx[0], b[1][1] - A1dx[1]
+    assert mod["dx"][1] == [r0, (r1 - 3 * r0) / 2]
