@@ -58,7 +58,8 @@ typedef enum {
 
 /* step flags */
 #define NS_REUSE_QR 1u    /* skip the QR of A_0, reuse the cached factors     */
-#define NS_NO_RESIDUAL 2u /* skip the residual norm ("can be omitted")          */
+#define NS_NO_RESIDUAL 2u /* skip the residual ("can be omitted"): no residual
+                             kernel; the returned ||b - A dx|| is 0                         */
 #define NS_LEDGER 4u      /* time the kernel classes with CUDA events (T4 classes)         */
 #define NS_TILED_BS 8u    /* per stage: y = Q^T b'_k then tiled back substitution (P:659-663,
                              P:124-126); default: dx_k = M b'_k with M = R^{-1} Q^T formed

@@ -41,6 +41,7 @@ ns_status step_impl(ns_system* s, double* x, double* res_out, uint32_t flags, cu
   // e4 end stage loop | e5 end residual.
   const bool ledger = (flags & NS_LEDGER) != 0;
   s->last_launches = 0;
+  s->no_resid = (flags & NS_NO_RESIDUAL) != 0;
   cudaEvent_t* ev = nullptr;
   if (ledger) {
     if (s->ledger_count == ns_system::LRING) {  // ring full: read the oldest record (rare)
@@ -496,6 +497,7 @@ ns_status ns_newton_series_step_from(ns_system* s, int precision, int dim, int d
   cudaStream_t st = (cudaStream_t)stream;
   const size_t K = s->K, d = s->d, n = s->n;
   s->last_launches = 0;
+  s->no_resid = (flags & NS_NO_RESIDUAL) != 0;
   CK(cudaMemcpyAsync(s->b, b, sizeof(double) * K * d * n, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(s->A, A, sizeof(double) * K * d * s->nnz, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(s->A0, A0, sizeof(double) * K * n * n, cudaMemcpyDeviceToDevice, st));
@@ -576,7 +578,7 @@ ns_status ns_run_newton(ns_system* s, int precision, int dim, int degree, double
   if (!s || !x || max_iter < 0) return NS_EINVAL;
   if (precision != s->K) return NS_EPREC;
   if (dim != s->n || degree != s->D) return NS_EDIM;
-  if (flags & ~(NS_QR_ONCE | NS_NO_STAGGER | NS_LEDGER | NS_TILED_BS)) return NS_EINVAL;
+  if (flags & ~(NS_QR_ONCE | NS_NO_STAGGER | NS_LEDGER | NS_TILED_BS | NS_NO_RESIDUAL)) return NS_EINVAL;
   CK(cudaSetDevice(s->dev));
   cudaStream_t st = (cudaStream_t)stream;
   const int K = s->K, d = s->d;
@@ -593,7 +595,7 @@ ns_status ns_run_newton(ns_system* s, int precision, int dim, int degree, double
     s->k_lo = k_lo;
     s->dc = dc;
     const bool refactor = qr_count == 0 || (k_lo == 0 && !(flags & NS_QR_ONCE));
-    uint32_t sf = (flags & (NS_LEDGER | NS_TILED_BS)) | (refactor ? 0u : NS_REUSE_QR);
+    uint32_t sf = (flags & (NS_LEDGER | NS_TILED_BS | NS_NO_RESIDUAL)) | (refactor ? 0u : NS_REUSE_QR);
     if (!refactor) sf &= ~NS_TILED_BS;  // the cached factorisation keeps its form
     else s->use_m = !(flags & NS_TILED_BS);
     if ((r = (cudaEventRecord(e0, st) == cudaSuccess) ? NS_OK : NS_ECUDA)) break;

@@ -51,7 +51,9 @@ template <int K>
 ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStream_t st) {
   // no memsets before the launch: the grid barrier is self-resetting and the
   // reflector flags carry an epoch (launch counter)
-  int epoch = ++s->qr_epoch;
+  // the epoch advances only with a launch that happened (the grid barrier's
+  // base is (epoch - 1) * grid: a failed launch must not skip an epoch)
+  int epoch = s->qr_epoch + 1;
   int n = s->n;
   const double* A0 = A0src;
   double *W = s->W, *vh = s->vhead, *be = s->beta, *rd = s->rdiag;
@@ -86,6 +88,7 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
     void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch, &ob};
     CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_kernel<K>, dim3(s->grid_qr), dim3(s->qr_threads),
                                    args, s->qr_smem_reserve, st));
+    s->qr_epoch = epoch;
     const long long tot = (long long)K * n * n;
     const int blocks = (int)std::min<long long>((tot + 255) / 256, 4LL * s->sms);
     ns::qr_unpack_kernel<K><<<blocks, 256, 0, st>>>(n, s->W, s->R, s->Qt);
@@ -151,16 +154,21 @@ ns_status launch_residual(ns_system* s, double* x, double* res_out, cudaStream_t
     const int* rl = s->n_sample ? s->sample_rows : nullptr;
     const long long rows = (long long)s->dc * nr;
     const int blocks = (int)std::max<long long>(1, std::min<long long>((rows + 7) / 8, 8LL * s->sms));
-    ns::residual_kernel<K><<<blocks, 256, 0, st>>>(s->n, s->d, s->dc, s->k_lo, rl, nr, s->b, s->bp, s->A0, s->dx,
-                                                   s->rbuf, s->knorm);
-    ns::knorm_kernel<K><<<s->dc, 128, 0, st>>>(s->n, s->d, s->k_lo, rl, nr, s->b, s->rbuf, s->dx, x, s->knorm);
+    // NS_NO_RESIDUAL ("can be omitted"): no residual kernel, ||r|| = 0
+    if (!s->no_resid) {
+      ns::residual_kernel<K><<<blocks, 256, 0, st>>>(s->n, s->d, s->dc, s->k_lo, rl, nr, s->b, s->bp, s->A0, s->dx,
+                                                     s->rbuf, s->knorm);
+      s->last_launches += 1;
+    }
+    ns::knorm_kernel<K><<<s->dc, 128, 0, st>>>(s->n, s->d, s->k_lo, rl, nr, s->b, s->no_resid ? nullptr : s->rbuf,
+                                               s->dx, x, s->knorm);
     s->last_launches += 1;
   }
   const long long tot = (long long)s->n * s->d;
   const int blocks = (int)std::max<long long>(1, std::min<long long>((tot + 255) / 256, 2LL * s->sms));
   ns::finalize_kernel<K><<<blocks, 256, 0, st>>>(s->n, s->d, s->dc, x, s->dx, s->knorm,
                                                  res_out ? res_out : s->res_tmp, s->status);
-  s->last_launches += 2;
+  s->last_launches += 1;
   CK(cudaGetLastError());
   return NS_OK;
 }
@@ -264,7 +272,16 @@ ns_status setup_grids(ns_system* s) {
       }
     }
   }
-  if (const char* e = getenv("NS_QR_GRID")) s->grid_qr = std::max(1, std::min(s->sms * occ, atoi(e)));
+  {
+    // co-residency bound of the grid QR at its real launch shape (threads and
+    // the reserving dynamic shared memory): an override can not exceed it
+    int occq = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occq, ns::householder_qr_kernel<K>, s->qr_threads,
+                                                     s->qr_smem_reserve));
+    if (occq < 1) return NS_ECUDA;
+    if (const char* e = getenv("NS_QR_GRID")) s->grid_qr = std::max(1, atoi(e));
+    s->grid_qr = std::min(s->grid_qr, s->sms * occq);
+  }
   s->st_threads = 256;
   if (const char* e = getenv("NS_STAGE_THREADS")) s->st_threads = atoi(e) >= 256 ? 256 : 128;
   s->stage_split = true;

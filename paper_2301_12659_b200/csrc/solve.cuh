@@ -706,7 +706,15 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
       r0 = s.row_ptr[row];
       len = s.row_ptr[row + 1] - r0;
     }
-    const bool cache = K < 8 && row < n && n <= 32 * RQ && len <= 32 * RQ;  // warp-uniform
+    // grid-uniform choice (every critical warp takes the same path, so every
+    // thread reaches the same sub_sync barrier instructions); warps without a
+    // row (row >= n) run the cached path with no loads and no stores
+    int maxlen = 0;
+    for (int r = lane; r < n; r += 32) maxlen = max(maxlen, s.row_ptr[r + 1] - s.row_ptr[r]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
+    const bool cache = K < 8 && n <= 32 * RQ && maxlen <= 32 * RQ;
+    const bool has_row = row < n;
     md::mdv<K> a1c[RQ], mc[RQ];
     int colc[RQ];
     if (cache) {
@@ -716,7 +724,7 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
         const int t = lane + 32 * q;
         a1c[q] = (t < len) ? md::load<K>(a.A + s.nnz, lsA, r0 + t) : md::zero<K>();
         colc[q] = (t < len) ? s.col_idx[r0 + t] : 0;
-        mc[q] = (t < n) ? md::load<K>(a.M, lsM, (long long)row * n + t) : md::zero<K>();
+        mc[q] = (has_row && t < n) ? md::load<K>(a.M, lsM, (long long)row * n + t) : md::zero<K>();
       }
     }
     for (int k = k_lo; k < dc; ++k) {
@@ -727,7 +735,7 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
       }
       if (trc) a.tr[4 * k + 1] = gtimer();
       if (cache) {
-        md::mdv<K> v = md::load_cg<K>(a.pend + (long long)k * n, lsV, row);
+        md::mdv<K> v = has_row ? md::load_cg<K>(a.pend + (long long)k * n, lsV, row) : md::zero<K>();
         if (k >= k_lo + 1) {
           const double* xp = a.dx + (long long)(k - 1) * n;
           md::mdv<K> xv[RQ];
@@ -746,7 +754,7 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
             }
           v = md::sub<K>(v, md::group_sum_levels<K>(sl, 32));
         }
-        if (lane == 0) md::store_cg<K>(a.bp + (long long)k * n, lsV, row, v);
+        if (lane == 0 && has_row) md::store_cg<K>(a.bp + (long long)k * n, lsV, row, v);
         sub_sync(a.cbar, target, a.Q);
         if (trc) a.tr[4 * k + 2] = gtimer();
         const double* bk = a.bp + (long long)k * n;
@@ -765,7 +773,7 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
             for (int l = 0; l < K; ++l) md::level_insert<K>(sl, l, pl[l]);
           }
         const md::mdv<K> acc = md::group_sum_levels<K>(sl, 32);
-        if (lane == 0) md::store_cg<K>(a.dx + (long long)k * n, lsV, row, acc);
+        if (lane == 0 && has_row) md::store_cg<K>(a.dx + (long long)k * n, lsV, row, acc);
         sub_sync(a.cbar, target, a.Q);
         if (trc) a.tr[4 * k + 3] = gtimer();
         if (blockIdx.x == 0 && threadIdx.x == 0) flag_set(a.ndx, k + 1);
@@ -819,6 +827,7 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
         // newly urgent pair behind the backlog of less urgent work)
         if (lane == 0 && ld_relaxed_s32(a.ndx) > avail) avail = ld_acquire(a.ndx);
         avail = __shfl_sync(0xffffffffu, avail, 0);
+        __syncwarp();  // orders the other lanes' dx loads after lane 0's acquire (a shuffle does not)
         const unsigned m = __ballot_sync(0xffffffffu, live && k_lo + pu / nch < avail);
         if (m == 0) {  // nothing available: wait for the next dx
           if (lane == 0) {
@@ -827,6 +836,7 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
             avail = ld_acquire(a.ndx);
           }
           avail = __shfl_sync(0xffffffffu, avail, 0);
+          __syncwarp();
           continue;
         }
         const int src = __ffs(m) - 1;
@@ -922,7 +932,9 @@ __global__ void __launch_bounds__(128) knorm_kernel(int n, int d, int k_lo, cons
   const long long lsV = (long long)d * n;
   const double* src = (w == 0) ? b : ((w == 1) ? rbuf : dx);
   md::mdv<K> acc = md::zero<K>();
-  const int cnt = (w == 1) ? nr : n;  // the residual norm runs over the sampled equations
+  // the residual norm runs over the sampled equations; rbuf = nullptr
+  // (NS_NO_RESIDUAL): no residual, its norm is 0
+  const int cnt = (w == 1) ? (rbuf ? nr : 0) : n;
   for (int t = lane; t < cnt; t += 32) {
     const int i = (w == 1 && rows) ? rows[t] : t;
     md::mdv<K> v = (w == 3) ? md::load<K>(x, lsV, (long long)i * d + k) : md::load<K>(src + (long long)k * n, lsV, i);

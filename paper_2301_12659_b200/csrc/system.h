@@ -61,6 +61,7 @@ struct ns_system {
   int* sflags = nullptr;       // [2d + 2] dx published, pend rows done, critical barrier  // dynamic smem requested by the QR kernel to own its SMs
   size_t ed_smem = 0;
   bool qr_cached = false;
+  bool no_resid = false;       // this step runs with NS_NO_RESIDUAL
   cudaStream_t last_stream = nullptr;
   // ledger
   static constexpr int LRING = 64;           // pending ledger records (6 events each)

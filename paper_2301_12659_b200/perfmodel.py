@@ -62,6 +62,32 @@ def step_counts(eq_ptr, mono_ptr, nnz: int, n: int, d: int, TB: int = 32) -> dic
                 stage=updates + qhb + bs, residual=resid, series_products=S)
 
 
+def algorithmic_counts(eq_ptr, mono_ptr, nnz: int, n: int, d: int) -> dict:
+    """The method's work per kernel class of one step (all orders 0..D), in md
+    multiply-adds, as SURVEY.md 8(a)/8(d) d.4 counts it -- independent of this
+    implementation's formulation (which factors [A0 | I] and forms
+    M = R^-1 Q^T once, so its own work differs):
+      evaldiff  S d(d+1)/2 triangular convolutions (3m-5 per monomial, no
+                padding) + (M + sum m) d coefficient scalings      (a2-a5)
+      qr        (2/3) n^3 Householder QR of A_0                     (a6)
+      stage     nnz d(d-1)/2 updates + 2 n^2 d for Q^T b (reflectors)
+                + n^2 d / 2 back substitution                      (a7-a9)
+      residual  nnz(A_0) d, the cheap form b'_k - A_0 dx_k           (a10)
+    """
+    M = len(mono_ptr) - 1
+    ms = [int(mono_ptr[t + 1] - mono_ptr[t]) for t in range(M)]
+    S = sum(products(m) for m in ms)
+    evaldiff = S * d * (d + 1) // 2 + (M + sum(ms)) * d
+    qr = (2 * n ** 3) // 3
+    updates = nnz * d * (d - 1) // 2
+    qhb = 2 * n * n * d
+    bs = n * n * d // 2
+    stage = updates + qhb + bs
+    residual = nnz * d
+    return dict(evaldiff=evaldiff, qr=qr, stage=stage, residual=residual, updates=updates, qhb=qhb, bs=bs,
+                series_products=S, total=evaldiff + qr + stage + residual)
+
+
 def flops(md_fma: int, K: int) -> int:
     return md_fma * mix_flops(MD_FMA_MIX[K])
 

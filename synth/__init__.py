@@ -25,6 +25,7 @@ float64 arrays [K][n][d]; coefficients [K][M]; CSR arrays int32.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -154,9 +155,37 @@ def _alpha_sum(alphas, vs) -> tuple[int, int]:
     return _sum_pairs(frac_pair(alphas[v]) for v in vs)
 
 
+def _rhs_exp_row(args):
+    """row i of the exp rhs: [K][d] (a pure function of its inputs; a worker)."""
+    Ss, cs, d, K = args
+    out = np.zeros((K, d))
+    for k in range(d):
+        terms = []
+        for (Sn, Sd), (cn, cd) in zip(Ss, cs):
+            en, ed = _exp_coeff_rational(Sn, Sd, k)
+            terms.append((cn * en, cd * ed))
+        num, den = _sum_pairs(terms)
+        out[:, k] = rational_to_md(num, den, K)
+    return out
+
+
+def _map_rows(fn, jobs):
+    """map over equations; in parallel worker processes when the exact
+    rational arithmetic is large (the configs C3/C4 take tens of seconds on
+    one core).  Same values either way (each row is computed by fn alone)."""
+    work = sum(len(j[0]) * j[2] * j[3] for j in jobs)  # (terms or coefficients) x d x K
+    import multiprocessing as mp
+    if work < 20000 or os.environ.get("SYNTH_SERIAL") or mp.current_process().daemon:
+        return [fn(j) for j in jobs]
+    ctx = mp.get_context("fork")
+    procs = min(len(jobs), max(1, len(os.sched_getaffinity(0))))
+    with ctx.Pool(procs) as pool:
+        return pool.map(fn, jobs, chunksize=max(1, len(jobs) // (4 * procs)))
+
+
 def _rhs_exp(eqs, coeffs, alphas, n, d, K) -> np.ndarray:
     """r_i,k = sum_tau c_tau S_tau^k / k!  (closed form of prod exp(alpha_j t))."""
-    rhs = np.zeros((K, n, d))
+    jobs = []
     t = 0
     for i, monos in enumerate(eqs):
         Ss = []
@@ -165,13 +194,11 @@ def _rhs_exp(eqs, coeffs, alphas, n, d, K) -> np.ndarray:
             Ss.append(_alpha_sum(alphas, vs))
             cs.append(_cpair(coeffs[t]))
             t += 1
-        for k in range(d):
-            terms = []
-            for (Sn, Sd), (cn, cd) in zip(Ss, cs):
-                en, ed = _exp_coeff_rational(Sn, Sd, k)
-                terms.append((cn * en, cd * ed))
-            num, den = _sum_pairs(terms)
-            rhs[:, i, k] = rational_to_md(num, den, K)
+        jobs.append((Ss, cs, d, K))
+    rows = _map_rows(_rhs_exp_row, jobs)
+    rhs = np.zeros((K, n, d))
+    for i, r in enumerate(rows):
+        rhs[:, i, :] = r
     return rhs
 
 
@@ -305,6 +332,9 @@ def make_x(system: System, kind: str = "near", seed: int = 1) -> np.ndarray:
     'start': x_0 = exact_0 (1 + u h), higher coefficients 0, h = HALF_PREC[K]
              ("x_0 with half its precision correct", P:498-501).
     'near':  every coefficient x_k = exact_k (1 + u_k h).
+    'rough': every coefficient x_k = exact_k (1 + u_k 2^-12): a step whose dx
+             is far above the tolerance at every k, so parity on dx is never
+             vacuous (tol_p s_k << |dx_k|).
     'int':   integer perturbation of the 1/(1-t) solution: x_{j,k} = 1 + (u in {0,1,2}).
     u ~ U[-1,1] from PCG64(seed).
     """
@@ -317,20 +347,33 @@ def make_x(system: System, kind: str = "near", seed: int = 1) -> np.ndarray:
         x[0] = 1.0 + vals
         return x
     u = rng.uniform(-1.0, 1.0, size=(n, d))
-    for j in range(n):
-        for k in range(d):
-            if kind == "start" and k > 0:
-                continue
-            en, ed = exact_coeff_rational(system, j, k)
-            if kind == "exact":
-                x[:, j, k] = rational_to_md(en, ed, K)
-                continue
-            un, ud = frac_pair(float(u[j, k]))
-            # exact_k * (1 + u h) = en (ud h_den + un h_num) / (ed ud h_den)
-            num = en * (ud * h_den + un * h_num)
-            den = ed * ud * h_den
-            x[:, j, k] = rational_to_md(num, den, K)
+    if kind == "rough":
+        h_num, h_den = 1, 2 ** 12
+    jobs = [([exact_coeff_rational(system, j, k) for k in range(d)], list(u[j]), d, K, kind, h_num, h_den)
+            for j in range(n)]
+    rows = _map_rows(_make_x_row, jobs)
+    for j, r in enumerate(rows):
+        x[:, j, :] = r
     return x
+
+
+def _make_x_row(args):
+    """series j of make_x: [K][d] (a worker; see make_x)."""
+    exact, u, d, K, kind, h_num, h_den = args
+    out = np.zeros((K, d))
+    for k in range(d):
+        if kind == "start" and k > 0:
+            continue
+        en, ed = exact[k]
+        if kind == "exact":
+            out[:, k] = rational_to_md(en, ed, K)
+            continue
+        un, ud = frac_pair(float(u[k]))
+        # exact_k * (1 + u h) = en (ud h_den + un h_num) / (ed ud h_den)
+        num = en * (ud * h_den + un * h_num)
+        den = ed * ud * h_den
+        out[:, k] = rational_to_md(num, den, K)
+    return out
 
 
 # --------------------------------------------------------------------------

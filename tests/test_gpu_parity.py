@@ -56,11 +56,16 @@ def _run_all(sys_, x_np):
                 rdiag=_np(rdiag), status=st.status_bits, pattern=h.pattern())
 
 
-def _full_parity(sys_, x_np, F, eps_cap=64.0):
+def _full_parity(sys_, x_np, F, eps_cap=64.0, out=None, nonvacuous=False):
+    """The whole step against the oracle (out: its result, computed here if
+    None).  nonvacuous: assert tol_p s_k < max_i |dx_k,i| at every k, i.e. a
+    wrong dx_k (even dx_k = 0) would fail the tolerance."""
     g = _run_all(sys_, x_np)
-    out = H.step_oracle(sys_, x_np, F)
+    if out is None:
+        out = H.step_oracle(sys_, x_np, F)
     n, d, K = sys_.n, sys_.d, sys_.K
-    ed = H.eval_diff_errors(sys_, x_np, g["b"], g["A"], list(range(n)), F, g["pattern"])
+    ed = H.eval_diff_errors(sys_, x_np, g["b"], g["A"], list(range(n)), F, g["pattern"],
+                            oracle_bA=(out["b"], out["A"]))
     assert ed["b"] <= 1 and ed["A"] <= 1, ed
     assert ed["b_eps"] <= eps_cap and ed["A_eps"] <= eps_cap, ed
     # dense A0 = structural A_0 scattered
@@ -71,6 +76,11 @@ def _full_parity(sys_, x_np, F, eps_cap=64.0):
             A0[:, i, ci[e]] = g["A"][:, 0, e]
     assert np.array_equal(A0, g["A0"])
     sv = H.solve_errors(sys_, x_np, out, g["dx"], F)
+    print(f"\n{sys_.name} n={n} d={d} K={K}: max err/(tol s) dx {sv['dx']:.2e}; per-k max err/(eps_p |x_k|): "
+          + " ".join(f"{v:.1e}" for v in sv["per_k_eps_x"]))
+    if nonvacuous:
+        vac = H.vacuity(out, sv["s"], synth.TOL_P[K])
+        assert max(vac) < 1.0, ("vacuous check at k =", [k for k, v in enumerate(vac) if v >= 1], vac)
     assert sv["dx"] <= 1, sv["dx"]
     assert sv["dx_eps"] <= eps_cap * n, sv["dx_eps"]
     xe = H.xnew_errors(sys_, x_np, out, g["x_new"], F, sv["s"])
@@ -265,11 +275,29 @@ def test_batched_matches_oracle_and_is_batch_invariant():
 
 # ------------------------------------------------------------------ full BASELINE sizes
 @pytest.mark.slow
-def test_C2_full_parity():
-    """configs[1]: dim=64, degree 31, quad double -- the whole step against the full oracle."""
+@pytest.mark.parametrize("kind", ["near", "start", "rough"])
+def test_C2_full_parity(kind):
+    """configs[1]: dim=64, degree 31, quad double -- the whole step against the
+    full oracle.  'start' (x_0 to half precision, the rest 0) and
+    'rough' (every coefficient perturbed by 2^-12) make dx large at every k,
+    so the tolerance tol_p s_k is asserted to be below |dx_k| (non-vacuous);
+    'near' (the timing input) is the near-converged case."""
     sys_ = synth.build_config("C2")
-    x = synth.make_x(sys_, "near", seed=1)
-    _full_parity(sys_, x, O.field_for(4))
+    x = synth.make_x(sys_, kind, seed=1)
+    F = O.field_for(4)
+    _full_parity(sys_, x, F, out=H.parallel_step(sys_, x, F), nonvacuous=(kind != "near"))
+
+
+@pytest.mark.slow
+def test_C3_full_parity_start():
+    """configs[2]: dim=128, degree 63, octo double, 'start' input: every
+    output of the step (b, A, dense A0, dx, x_new, norms) against the full
+    oracle (parallel_step: the oracle's own functions over worker processes),
+    non-vacuous at every k."""
+    sys_ = synth.build_config("C3")
+    x = synth.make_x(sys_, "start", seed=1)
+    F = O.field_for(8)
+    _full_parity(sys_, x, F, out=H.parallel_step(sys_, x, F), nonvacuous=True)
 
 
 @pytest.mark.slow
@@ -369,3 +397,94 @@ def test_sharded_evaldiff_rows_bitwise_and_step_from():
     res = torch.zeros((4, 3), dtype=torch.float64, device="cuda:0")
     full.step_from(x2, bs, As, A0s, res)
     assert H.xnew_errors(sys_, x_np, out, _np(x2), F, s_k) <= 1
+
+
+# ------------------------------------------------------------------ C4 shape and the large-n code paths
+class _env:
+    """environment overrides read by ns_system_create (launch-shape knobs)"""
+
+    def __init__(self, **kw):
+        self.kw = kw
+
+    def __enter__(self):
+        import os
+        self.old = {k: os.environ.get(k) for k in self.kw}
+        os.environ.update({k: str(v) for k, v in self.kw.items()})
+
+    def __exit__(self, *a):
+        import os
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("split", [1, 0])
+def test_n160_grid_qr_streaming_and_stage_paths(split):
+    """n = 160 > 128: the grid QR's rows beyond its 32 S register window are
+    streamed from L2, and (split = 0) the non-split stage_kernel that C4
+    (n = 1024) runs; 2-column banded system with signed md coefficients
+    (the C4 structure at w = 32), 'rough' input: full oracle parity."""
+    sys_ = synth.banded_two_column_system(160, 32, 15, 4, seed=44)
+    x = synth.make_x(sys_, "rough", seed=45)
+    F = O.field_for(4)
+    out = H.parallel_step(sys_, x, F)
+    with _env(NS_STAGE_SPLIT=split):
+        _full_parity(sys_, x, F, out=out, nonvacuous=True)
+
+
+@pytest.mark.parametrize("owner", [0, 1])
+def test_grid_qr_owner_beta_modes(owner):
+    """NS_QR_OWNER_BETA: the reflector's owner forms beta (1, default) or each
+    consumer forms it (0); both within tol_p s_k of the oracle."""
+    sys_ = synth.triangular_system(40, 12, 8, seed=47)
+    x = synth.make_x(sys_, "rough", seed=48)
+    with _env(NS_QR_OWNER_BETA=owner):
+        _full_parity(sys_, x, O.field_for(8), nonvacuous=True)
+
+
+@pytest.mark.slow
+def test_C4_sampled_rows_and_a_posteriori_residual():
+    """configs[3] at full size (n = 1024, w = 32, degree 31, 4d), 'rough' input.
+    (1) b and A on sampled equations against the oracle (SURVEY d.6);
+    (2) the GPU dx solves the block system: on those equations the residual
+    r_k,i = b_k,i - sum_{j<=k} (A_j dx_{k-j})_i, evaluated exactly on the
+    GPU's verified A, b and its dx, is within tol_p times the normwise scale
+    max_i' (|b_k| + sum_j |A_j| |dx_{k-j}|)_i' (Householder QR is normwise
+    backward stable, reading R33), and that bound is far below |b_k| on those
+    rows (a wrong dx, e.g. 0, fails); (3) the step's x_new = x + dx of the
+    solve bit for bit."""
+    sys_ = synth.build_config("C4")
+    x = synth.make_x(sys_, "rough", seed=1)
+    g = _run_all(sys_, x)
+    F = O.field_for(4)
+    rows = [0, 1, 31, 32, 500, 511, 512, 1022, 1023]
+    ob, oA = H.parallel_rows(sys_, x, F, rows)
+    ed = H.eval_diff_errors(sys_, x, g["b"], g["A"], rows, F, g["pattern"], oracle_bA=(ob, oA))
+    assert ed["b"] <= 1 and ed["A"] <= 1, ed
+    rp, ci = g["pattern"]
+    K, d = 4, sys_.d
+    tol = synth.TOL_P[K]
+    Aab, dxab, bab = np.abs(g["A"][0]), np.abs(g["dx"][0]), np.abs(g["b"][0])
+    worst = 0.0
+    for k in range(d):
+        rowscale = bab[k].copy()
+        for j in range(k + 1):
+            rowscale += np.add.reduceat(Aab[j] * dxab[k - j][ci], rp[:-1]) * (np.diff(rp) > 0)
+        scale_k = Fraction(float(rowscale.max()))
+        assert max(bab[k][i] for i in rows) > 1e6 * tol * float(scale_k)  # non-vacuous
+        for i in rows:
+            r = H.limbs_to_fraction(g["b"][:, k, i])
+            for j in range(k + 1):
+                for e in range(rp[i], rp[i + 1]):
+                    r -= H.limbs_to_fraction(g["A"][:, j, e]) * H.limbs_to_fraction(g["dx"][:, k - j, ci[e]])
+            worst = max(worst, float(abs(r) / scale_k) / tol)
+    print(f"\nC4 a-posteriori residual: max |r| / (tol_p scale) = {worst:.2e}")
+    assert worst <= 1, worst
+    xn = g["x_new"]
+    for i in rows:
+        for k in (0, 7, d - 1):
+            want = H.limbs_to_fraction(x[:, i, k]) + H.limbs_to_fraction(g["dx"][:, k, i])
+            assert abs(H.limbs_to_fraction(xn[:, i, k]) - want) <= Fraction(tol) * abs(want)
