@@ -442,16 +442,23 @@ def extra_c4(args, local, dev, flush, peak, K=4, reuse=False):
     import paper_2301_12659_b200 as P
     import synth
     from paper_2301_12659_b200 import perfmodel as PM
-    from paper_2301_12659_b200.dist import equation_partition, replicate_rows
     ws, rank, _ = dist_env()
     sys_ = synth.build_config("C4", K=K)
     x_np = synth.make_x(sys_, "near", seed=1)
     h = P.NewtonSystem.from_system(sys_, device=local)
-    ranges = equation_partition(sys_.eq_ptr, sys_.mono_ptr, sys_.d, ws)
-    lo, hi = ranges[rank]
     if ws > 1:
-        h.set_partition(lo, hi)
-    rp, _ = h.pattern()
+        # the library owns the communicator: rank 0's NCCL id goes to every rank
+        # (torch.distributed is the bootstrap only); from then on the step
+        # shards eval/diff and replicates the rows inside the library
+        import torch.distributed as tdist
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(P.nccl_unique_id()), dtype=torch.uint8))
+        tdist.broadcast(uid, src=0)
+        h.comm_init(ws, rank, bytes(uid.cpu().numpy().tobytes()))
+    bounds, _ = P.exchange_plan(sys_.eq_ptr, sys_.mono_ptr, sys_.var_idx, sys_.n,
+                                                                    sys_.D, sys_.K, ws)
+    ranges = [(int(bounds[r]), int(bounds[r + 1])) for r in range(ws)]
     x0 = torch.tensor(x_np, device=dev)
     x = x0.clone()
     res = torch.zeros((K, 3), dtype=torch.float64, device=dev)
@@ -459,12 +466,7 @@ def extra_c4(args, local, dev, flush, peak, K=4, reuse=False):
     stream = torch.cuda.current_stream()
 
     def one(flags):
-        if ws == 1:
-            h.step(x, res, flags=flags)
-            return
-        b, A, A0 = h.eval_diff(x)
-        replicate_rows(b, A, A0, rp, ranges, rank)
-        h.step_from(x, b, A, A0, res, flags=flags)
+        h.step(x, res, flags=flags)
 
     for _ in range(max(args.warmup, 2)):
         x.copy_(x0)
@@ -483,7 +485,8 @@ def extra_c4(args, local, dev, flush, peak, K=4, reuse=False):
     ms = max_ranks(sum(a.elapsed_time(b) for a, b in ev) / steps, dev)
     tot = counts["total"] - (counts["qr"] if reuse else 0)
     g = PM.flops(tot, K) / (ms * 1e-3) * 1e-9
-    return {"workload": workload_desc("C4", sys_) + f"; eval/diff sharded by equations over {ws} GPU(s)",
+    return {"workload": workload_desc("C4", sys_) + f"; eval/diff sharded by equations over {ws} GPU(s), rows "
+                        "replicated by the library's grouped ncclBroadcast, solve replicated",
             "ranges": ranges, "reuse_qr": reuse, "ms_per_step": ms, "gflops": g,
             "pct_of_peak": 100 * g / (ws * peak["gflops"]), "scaling": "strong"}
 

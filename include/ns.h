@@ -110,7 +110,13 @@ typedef struct {
 } ns_run_info;
 
 /* kernel classes of T4; updates, qhb and bs are fused into one
- * persistent stage kernel and reported together as "stage" */
+ * persistent stage kernel and reported together as "stage".  Like the
+ * paper's ledger, operation counts accumulate beside the times:
+ * the algorithmic md multiply-adds of each class (triangular
+ * convolutions + coefficient scalings; (2/3) n^3 for the QR; nnz d(d-1)/2
+ * updates + 2 n^2 d for Q^T b + n^2 d / 2 back substitution; nnz d for the
+ * residual; over the active window), and the FP64 flops they cost in this
+ * library's md arithmetic (static DADD/DMUL/DFMA counts of md.cuh, FMA = 2). */
 typedef struct {
   double ms_convolution; /* eval/diff (side stream, concurrent with the QR) */
   double ms_qr;          /* A_0 + Householder QR + tile inverses + M       */
@@ -119,6 +125,9 @@ typedef struct {
   double ms_total;       /* whole step (start to end, the overlap included) */
   int64_t steps;         /* ledger steps accumulated                     */
   int64_t qr_count;      /* QR factorisations performed                  */
+  int64_t md_fma_convolution, md_fma_qr, md_fma_stage, md_fma_residual; /* md multiply-adds */
+  double flops_per_md_fma; /* FP64 flops of one md multiply-add (K = 2: 18, 4: 166, 8: 1176) */
+  double fp64_flops;       /* sum of the md_fma counts x flops_per_md_fma               */
 } ns_ledger;
 
 /* Create a handle for one system on CUDA device cuda_device; validates the
@@ -148,6 +157,42 @@ ns_status ns_newton_series_step_batched(ns_system* sys, int precision, int dim, 
  * ns_newton_series_step_from on every rank.  NS_EINVAL for an empty or
  * out-of-range partition; synchronises the handle's device. */
 ns_status ns_set_partition(ns_system* sys, int eq_lo, int eq_hi);
+/* Multi-GPU, one large system (north_star "convolution
+ * jobs ... followed by an NCCL reduction ... over NVLink").  The library owns
+ * the NCCL communicator.  Bootstrap: rank 0 calls ns_nccl_unique_id, the
+ * caller broadcasts the 128 bytes (torch.distributed), every rank calls
+ * ns_comm_init with its own handle of the same system on its own GPU.  From
+ * then on ns_newton_series_step on every rank evaluates and differentiates
+ * only the rank's equations (the contiguous ranges of ns_exchange_plan,
+ * balanced by convolution cost), replicates the rows of b, A and A_0 of every
+ * rank with one grouped ncclBroadcast per rank block (rows are copied, never
+ * summed: no ncclSum on limb planes, so every rank's step is bitwise the
+ * one-GPU step), and runs the QR, stage loop and residual replicated.  All of
+ * it on the step's stream; no host synchronisation.  Collective: every rank
+ * must make the same sequence of step calls.  Loads libnccl.so.2 at run time
+ * (the copy already in the process, else NS_NCCL_LIB or the loader path);
+ * NS_ENCCL if it can not.  ns_comm_init: NS_EINVAL for a bad rank / nranks
+ * (nranks <= dim), NS_ESTATE inside a staggered window, NS_ENOMEM, NS_ENCCL;
+ * it synchronises the device and blocks until all ranks joined.
+ * ns_eval_diff on a sharded handle computes the rank's rows only. */
+ns_status ns_nccl_unique_id(void* uid128);
+ns_status ns_comm_init(ns_system* sys, int nranks, int rank, const void* uid128);
+/* Host only (no device, no handle): for the system of `desc`, the equation
+ * ranges eq_bounds[nranks + 1] of the partition ns_comm_init uses, and the
+ * size in doubles of each rank's block (block_doubles may be NULL).  Block
+ * layout (the row replication contract): [b rows: for l < K, k < d:
+ * b[l][k][lo..hi)] [A entries: for l, k: A[l][k][row_ptr[lo]..row_ptr[hi])]
+ * [A_0 rows: for l: A_0[l][lo..hi][0..n)]. */
+ns_status ns_exchange_plan(const ns_system_desc* desc, int nranks, int32_t* eq_bounds, int64_t* block_doubles);
+/* The pack / unpack kernel of the replication (device arrays, layouts as
+ * above): unpack = 0 copies rows [lo, hi) of (b, A, A0) into block, unpack = 1
+ * copies block into those rows.  Asynchronous on stream. */
+ns_status ns_pack_rows(const ns_system* sys, int lo, int hi, double* b, double* A, double* A0, double* block,
+                       int unpack, void* stream);
+/* NCCL asynchronous error of the handle's communicator (0 = none; NS_ENCCL
+ * when set).  NS_OK without a communicator. */
+ns_status ns_comm_status(ns_system* sys, int32_t* nccl_async_error);
+
 /* The step after eval/diff: QR of the given A0, stage loop, residual and
  * x += dx, for (b, A, A0) computed elsewhere (all device, layouts as above). */
 ns_status ns_newton_series_step_from(ns_system* sys, int precision, int dim, int degree, double* x_series,

@@ -37,7 +37,8 @@ EXPORTS = ["ns_system_create", "ns_system_destroy", "ns_newton_series_step",
            "ns_fp64_peak_probe", "ns_md_latency_probe", "ns_barrier_probe", "ns_set_partition",
            "ns_newton_series_step_from", "ns_get_trace", "ns_get_qr_trace", "ns_set_window",
            "ns_get_stage_norms", "ns_run_newton", "ns_get_stage_trace",
-           "ns_set_residual_sample", "ns_fabry_ratio"]
+           "ns_set_residual_sample", "ns_fabry_ratio", "ns_nccl_unique_id", "ns_comm_init",
+           "ns_exchange_plan", "ns_comm_status", "ns_pack_rows"]
 
 
 class NSError(RuntimeError):
@@ -77,7 +78,10 @@ class RunInfo(ctypes.Structure):
 class Ledger(ctypes.Structure):
     _fields_ = [("ms_convolution", ctypes.c_double), ("ms_qr", ctypes.c_double),
                 ("ms_stage", ctypes.c_double), ("ms_residual", ctypes.c_double), ("ms_total", ctypes.c_double),
-                ("steps", ctypes.c_int64), ("qr_count", ctypes.c_int64)]
+                ("steps", ctypes.c_int64), ("qr_count", ctypes.c_int64),
+                ("md_fma_convolution", ctypes.c_int64), ("md_fma_qr", ctypes.c_int64),
+                ("md_fma_stage", ctypes.c_int64), ("md_fma_residual", ctypes.c_int64),
+                ("flops_per_md_fma", ctypes.c_double), ("fp64_flops", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -109,6 +113,11 @@ def lib() -> ctypes.CDLL:
         "ns_get_stage_trace": ([vp, vp], i32),
         "ns_set_residual_sample": ([vp, vp, ctypes.c_int], ctypes.c_int),
         "ns_fabry_ratio": ([vp, vp, vp, vp], ctypes.c_int),
+        "ns_nccl_unique_id": ([vp], ctypes.c_int),
+        "ns_comm_init": ([vp, ctypes.c_int, ctypes.c_int, vp], ctypes.c_int),
+        "ns_exchange_plan": ([ctypes.POINTER(_Desc), ctypes.c_int, vp, vp], ctypes.c_int),
+        "ns_pack_rows": ([vp, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, ctypes.c_int, vp], ctypes.c_int),
+        "ns_comm_status": ([vp, vp], ctypes.c_int),
         "ns_newton_series_step_from": ([vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, u32, vp],
                                        ctypes.c_int),
         "ns_set_window": ([vp, ctypes.c_int, ctypes.c_int], ctypes.c_int),
@@ -264,7 +273,24 @@ class NewtonSystem:
         _check(lib().ns_fabry_ratio(self._h, _ptr(x), _ptr(z), _stream_ptr(stream)), "ns_fabry_ratio")
         return z
 
-    # ---- sharded eval/diff (C4)
+    # ---- one system over N GPUs: library-owned NCCL communicator (C4)
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        """ns_comm_init: from now on step() shards eval/diff by equations and
+        replicates the rows over NCCL inside the library (collective)."""
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        _check(lib().ns_comm_init(self._h, nranks, rank, buf), "ns_comm_init")
+
+    def pack_rows(self, lo: int, hi: int, b, A, A0, block, unpack: bool = False, stream=None):
+        """ns_pack_rows: rows [lo, hi) of (b, A, A0) <-> one replication block."""
+        _check(lib().ns_pack_rows(self._h, lo, hi, _ptr(b), _ptr(A), _ptr(A0), _ptr(block), 1 if unpack else 0,
+                                  _stream_ptr(stream)), "ns_pack_rows")
+
+    def comm_status(self) -> int:
+        e = ctypes.c_int32()
+        lib().ns_comm_status(self._h, ctypes.byref(e))
+        return e.value
+
+    # ---- sharded eval/diff (C4), caller-driven variant
     def set_partition(self, eq_lo: int, eq_hi: int):
         """ns_set_partition: this handle's eval/diff computes rows [eq_lo, eq_hi)."""
         _check(lib().ns_set_partition(self._h, eq_lo, eq_hi), "ns_set_partition")
@@ -361,6 +387,26 @@ def md_op(precision: int, op: str, a, b=None, c=None, stream=None):
         c = torch.zeros_like(a)
     _check(lib().ns_md_op(precision, code, n, _ptr(a), _ptr(b), _ptr(c), _stream_ptr(stream)), "ns_md_op")
     return c
+
+
+def exchange_plan(eq_ptr, mono_ptr, var_idx, dim: int, degree: int, precision: int, nranks: int):
+    """ns_exchange_plan (host only, no GPU): equation bounds [nranks+1] of the
+    partition and each rank's replication block size in doubles [nranks]."""
+    e = np.ascontiguousarray(eq_ptr, np.int32)
+    m = np.ascontiguousarray(mono_ptr, np.int32)
+    v = np.ascontiguousarray(var_idx, np.int32)
+    desc = _Desc(dim, degree, precision, len(m) - 1, 1, e.ctypes.data, m.ctypes.data, v.ctypes.data, None, None)
+    b = np.zeros(nranks + 1, np.int32)
+    c = np.zeros(nranks, np.int64)
+    _check(lib().ns_exchange_plan(ctypes.byref(desc), nranks, b.ctypes.data, c.ctypes.data), "ns_exchange_plan")
+    return b, c
+
+
+def nccl_unique_id() -> bytes:
+    """ns_nccl_unique_id: 128 bytes for ns_comm_init (rank 0; broadcast by the caller)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().ns_nccl_unique_id(buf), "ns_nccl_unique_id")
+    return buf.raw
 
 
 def build_info() -> str:

@@ -14,7 +14,7 @@ BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
-UNITS = ["api.cu", "kernels_k2.cu", "kernels_k4.cu", "kernels_k8.cu"]
+UNITS = ["api.cu", "comm.cu", "kernels_k2.cu", "kernels_k4.cu", "kernels_k8.cu"]
 
 
 def _deps_mtime() -> float:
@@ -40,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(len(UNITS)) as ex:
         objs = list(ex.map(one, UNITS))
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT, *objs]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

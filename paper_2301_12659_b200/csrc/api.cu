@@ -33,6 +33,26 @@ int cost_of_eq(const ns_system* s, int i) {
 
 ns_status collect_one(ns_system* s);
 
+// FP64 flops of one md multiply-add of md.cuh (static counts; perfmodel.MD_FMA_MIX)
+double md_fma_flops(int K) { return K == 2 ? 18.0 : (K == 4 ? 166.0 : 1176.0); }
+
+// algorithmic md multiply-adds of one step on the window [k_lo, dc) (include/ns.h ns_ledger)
+void ledger_counts(ns_system* s, bool qr) {
+  const long long n = s->n, dc = s->dc, kl = s->k_lo, nnz = s->nnz;
+  const long long conv = s->series_products * dc * (dc + 1) / 2 + s->scale_terms * dc;
+  long long upd = 0;
+  for (long long k = kl; k < dc; ++k) upd += nnz * (k - kl);
+  const long long st = upd + (dc - kl) * (2 * n * n + n * n / 2);
+  const long long qrc = qr ? 2 * n * n * n / 3 : 0;
+  const long long res = nnz * (dc - kl);
+  s->ledger.md_fma_convolution += conv;
+  s->ledger.md_fma_qr += qrc;
+  s->ledger.md_fma_stage += st;
+  s->ledger.md_fma_residual += res;
+  s->ledger.flops_per_md_fma = md_fma_flops(s->K);
+  s->ledger.fp64_flops += md_fma_flops(s->K) * (double)(conv + qrc + st + res);
+}
+
 template <int K>
 ns_status step_impl(ns_system* s, double* x, double* res_out, uint32_t flags, cudaStream_t st) {
   // Fork: eval/diff on the side stream; on the caller's stream A_0 alone
@@ -63,6 +83,11 @@ ns_status step_impl(ns_system* s, double* x, double* res_out, uint32_t flags, cu
   if (ledger) CK(cudaEventRecord(ev[2], st));
   r = Impl<K>::evaldiff(s, x, s->side);
   if (r) return r;
+  // sharded eval/diff (ns_comm_init): replicate every rank's rows over NVLink
+  if (ns_comm_active(s)) {
+    r = ns_comm_exchange(s, s->side);
+    if (r) return r;
+  }
   if (ledger) CK(cudaEventRecord(ev[1], s->side));
   CK(cudaEventRecord(s->ev_join, s->side));
   CK(cudaStreamWaitEvent(st, s->ev_join, 0));
@@ -76,6 +101,7 @@ ns_status step_impl(ns_system* s, double* x, double* res_out, uint32_t flags, cu
     CK(cudaEventRecord(ev[5], st));
     s->ledger_count += 1;
     if (!(flags & NS_REUSE_QR)) s->ledger.qr_count += 1;
+    ledger_counts(s, !(flags & NS_REUSE_QR));
   }
   s->last_stream = st;
   return NS_OK;
@@ -125,10 +151,12 @@ void free_all(ns_system* s) {
   if (s->side) cudaStreamDestroy(s->side);
 }
 
+}  // namespace
+
 // Job list of the eval/diff job queue for the equations [eq_lo, eq_hi): chains
 // longest first (LPT), cross products by the layer their inputs appear at,
 // equations by their longest monomial.  ser_off / left cover all monomials.
-void build_jobs(const ns_system* s, int eq_lo, int eq_hi, std::vector<int4>& jobs, std::vector<long long>& ser_off,
+void ns_build_jobs(const ns_system* s, int eq_lo, int eq_hi, std::vector<int4>& jobs, std::vector<long long>& ser_off,
                 std::vector<int>& left, long long& pool_series) {
   const int M = s->M;
   std::vector<int4> chains, cross, eqs;
@@ -160,6 +188,8 @@ void build_jobs(const ns_system* s, int eq_lo, int eq_hi, std::vector<int4>& job
   jobs.insert(jobs.end(), cross.begin(), cross.end());
   jobs.insert(jobs.end(), eqs.begin(), eqs.end());
 }
+
+namespace {
 
 }  // namespace
 
@@ -220,6 +250,11 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   s->M = M;
   s->m_max = m_max;
   s->max_batch = std::max(1, desc->max_batch);
+  for (int t = 0; t < M; ++t) {
+    const int m = desc->mono_ptr[t + 1] - desc->mono_ptr[t];
+    s->series_products += (m <= 1) ? 0 : (m == 2 ? 1 : 3 * m - 5);
+    s->scale_terms += 1 + m;
+  }
   s->TB = 32;
   s->T = (n + s->TB - 1) / s->TB;
   const int L = desc->mono_ptr[M];
@@ -256,7 +291,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   std::vector<long long> ser_off;
   std::vector<int> left;
   long long pool_series = 0;
-  build_jobs(s, 0, n, jobs, ser_off, left, pool_series);
+  ns_build_jobs(s, 0, n, jobs, ser_off, left, pool_series);
   s->njobs = (int)jobs.size();
   s->njobs_full = s->njobs;
 
@@ -368,6 +403,7 @@ void ns_system_destroy(ns_system* s) {
   if (!s) return;
   cudaSetDevice(s->dev);
   cudaDeviceSynchronize();
+  ns_comm_free(s);
   free_all(s);
   if (s->cqr_trace) cudaFree(s->cqr_trace);
   delete s;
@@ -476,7 +512,7 @@ ns_status ns_set_partition(ns_system* s, int eq_lo, int eq_hi) {
   std::vector<long long> ser_off;
   std::vector<int> left;
   long long pool_series = 0;
-  build_jobs(s, eq_lo, eq_hi, jobs, ser_off, left, pool_series);
+  ns_build_jobs(s, eq_lo, eq_hi, jobs, ser_off, left, pool_series);
   CK(cudaSetDevice(s->dev));
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(s->jobs, jobs.data(), sizeof(int4) * jobs.size(), cudaMemcpyHostToDevice));
@@ -716,6 +752,7 @@ ns_status ns_reset_ledger(ns_system* s) {
   ns_status r = collect_ledger(s);
   if (r) return r;
   s->ledger = ns_ledger{};
+  s->ledger.flops_per_md_fma = md_fma_flops(s->K);
   return NS_OK;
 }
 

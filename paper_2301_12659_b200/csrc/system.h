@@ -6,6 +6,8 @@
 
 #include "../../include/ns.h"
 
+struct ns_comm;  // comm.cu
+
 struct ns_system {
   int dev = 0;
   int n = 0, D = 0, d = 0, K = 0, M = 0, nnz = 0, m_max = 0, max_batch = 1;
@@ -75,12 +77,24 @@ struct ns_system {
   int ledger_head = 0, ledger_count = 0;     // ring of steps whose events are not yet read
   ns_ledger ledger{};
   int last_launches = 0;
+  long long series_products = 0, scale_terms = 0;  // S = sum (3m-5), M + sum m (ledger counts)
+  ns_comm* comm = nullptr;     // ns_comm_init (comm.cu), nullptr: one GPU
   // batched
   double* bws = nullptr;
   size_t bws_per_path = 0;
   size_t batched_smem = 0;
 };
 
+
+// eval/diff job list of the equations [eq_lo, eq_hi) (api.cu)
+void ns_build_jobs(const ns_system* s, int eq_lo, int eq_hi, std::vector<int4>& jobs, std::vector<long long>& ser_off,
+                   std::vector<int>& left, long long& pool_series);
+
+// multi-GPU exchange (comm.cu): library-owned NCCL communicator, equation
+// partition, row replication of b, A, A_0 after the sharded eval/diff
+ns_status ns_comm_exchange(ns_system* s, cudaStream_t st);  // pack own rows, grouped broadcasts, unpack
+void ns_comm_free(ns_system* s);
+bool ns_comm_active(const ns_system* s);
 
 // per-precision entry points, defined in kernels_k{2,4,8}.cu (impl.cuh)
 template <int K>

@@ -114,3 +114,91 @@ def test_gloo_world2_row_replication_bitwise():
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok in out), out
+
+
+# ------------------------------------------------------------------ C4: the library's row replication plan
+def _c4_like(n=40, w=6, D=5, K=4):
+    import synth
+    return synth.banded_two_column_system(n, w, D, K, seed=3)
+
+
+def test_exchange_plan_through_c_abi_matches_partition():
+    """ns_exchange_plan (host only, through the C ABI) gives the equation
+    ranges of dist.equation_partition and the block sizes of the layout
+    contract in include/ns.h: K (d (rows + entries) + rows n)."""
+    import numpy as np
+
+    import paper_2301_12659_b200 as P
+    from oracle import newton as O
+    from paper_2301_12659_b200.dist import equation_partition
+    for sys_ in (_c4_like(), _c4_like(64, 32, 31, 4), _c4_like(9, 3, 2, 2)):
+        rp = np.cumsum([0] + [len(r) for r in O.jacobian_pattern(sys_)])
+        for world in (1, 2, 3, 8):
+            if world > sys_.n:
+                continue
+            b, c = P.exchange_plan(sys_.eq_ptr, sys_.mono_ptr, sys_.var_idx, sys_.n, sys_.D, sys_.K, world)
+            ranges = equation_partition(sys_.eq_ptr, sys_.mono_ptr, sys_.d, world)
+            assert [(int(b[r]), int(b[r + 1])) for r in range(world)] == ranges
+            for r, (lo, hi) in enumerate(ranges):
+                assert c[r] == sys_.K * (sys_.d * ((hi - lo) + (rp[hi] - rp[lo])) + (hi - lo) * sys_.n)
+
+
+def _pack(b, A, A0, rp, lo, hi):
+    """the block layout of include/ns.h (ns_exchange_plan), restated in numpy"""
+    import numpy as np
+    return np.concatenate([b[:, :, lo:hi].reshape(-1), A[:, :, rp[lo]:rp[hi]].reshape(-1), A0[:, lo:hi, :].reshape(-1)])
+
+
+def _unpack(blk, b, A, A0, rp, lo, hi):
+    K, d, n = b.shape
+    nb, na = K * d * (hi - lo), K * d * (rp[hi] - rp[lo])
+    b[:, :, lo:hi] = blk[:nb].reshape(K, d, hi - lo)
+    A[:, :, rp[lo]:rp[hi]] = blk[nb:nb + na].reshape(K, d, rp[hi] - rp[lo])
+    A0[:, lo:hi, :] = blk[nb + na:].reshape(K, hi - lo, n)
+
+
+def _replicate_worker(rank, world, port, q):
+    import numpy as np
+
+    import paper_2301_12659_b200 as P
+    from oracle import newton as O
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys_ = _c4_like()
+    K, d, n = sys_.K, sys_.d, sys_.n
+    rp = np.cumsum([0] + [len(r) for r in O.jacobian_pattern(sys_)])
+    rng = np.random.default_rng(17)                       # the same "evaluated" arrays on every rank
+    fb, fA, f0 = rng.random((K, d, n)), rng.random((K, d, int(rp[-1]))), rng.random((K, n, n))
+    bounds, cnt = P.exchange_plan(sys_.eq_ptr, sys_.mono_ptr, sys_.var_idx, n, sys_.D, K, world)
+    off = np.concatenate([[0], np.cumsum(cnt)])
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    b, A, A0 = np.zeros_like(fb), np.zeros_like(fA), np.zeros_like(f0)   # this rank's rows only
+    b[:, :, lo:hi], A[:, :, rp[lo]:rp[hi]], A0[:, lo:hi] = fb[:, :, lo:hi], fA[:, :, rp[lo]:rp[hi]], f0[:, lo:hi]
+    gather = torch.zeros(int(off[-1]), dtype=torch.float64)
+    gather[off[rank]:off[rank + 1]] = torch.from_numpy(_pack(b, A, A0, rp, lo, hi))
+    for r in range(world):                                # the grouped broadcast, one root per block
+        seg = gather[off[r]:off[r + 1]].clone()
+        dist.broadcast(seg, src=r)
+        gather[off[r]:off[r + 1]] = seg
+    for r in range(world):
+        if r != rank:
+            _unpack(gather[off[r]:off[r + 1]].numpy(), b, A, A0, rp, int(bounds[r]), int(bounds[r + 1]))
+    q.put((rank, bool((b == fb).all() and (A == fA).all() and (A0 == f0).all())))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_row_replication_plan():
+    """The library's exchange (ns_comm_init path) on CPU: the plan from the
+    C ABI, each rank's rows packed in the contract layout, one broadcast per
+    root block over gloo, unpacked: every rank ends with every row, bitwise."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_replicate_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=180) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in out), out

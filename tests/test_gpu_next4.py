@@ -89,3 +89,35 @@ def test_residual_sampling(rows):
     assert abs(H.limbs_to_fraction(samp[:, 1]) - want) <= bound
     if rows == list(range(8)):
         assert np.array_equal(full[:, 1], samp[:, 1])  # same rows, same order
+
+
+@pytest.mark.parametrize("rows", [[0], [1, 5, 7], [6, 2]])
+def test_residual_sampling_nonzero_residual(rows):
+    """Non-vacuous sampling parity: a step with a stale factorisation
+    (NS_REUSE_QR after factoring the A_0 of another x_0, the modified Newton
+    of P:665-668) has r_k = b'_k - A_0 dx_k != 0, so the sampled norm
+    depends on which equations are selected.  Against the oracle's
+    step_window(x0_factor=...) residual on the same rows (exact rationals)."""
+    import torch
+
+    import paper_2301_12659_b200 as P
+    sys_ = synth.build_config("C1")
+    xf = synth.make_x(sys_, "rough", seed=31)
+    x_np = synth.make_x(sys_, "rough", seed=32)
+    h = _handle(sys_)
+    h.step(torch.tensor(xf, device="cuda:0"))                    # caches the factors of A_0(xf)
+    h.set_residual_sample(rows)
+    x = torch.tensor(x_np, device="cuda:0")
+    res = torch.zeros((sys_.K, 3), dtype=torch.float64, device="cuda:0")
+    h.step(x, res, flags=P.NS_REUSE_QR)
+    h.set_residual_sample(None)
+    got = H.limbs_to_fraction(res.cpu().numpy()[:, 1])
+    F = O.ExactField()
+    out = O.step_window(sys_, x_np, F, 0, sys_.d, x0_factor=xf)
+    want = O.residual_norm_sampled(out["r"], rows)
+    others = [O.residual_norm_sampled(out["r"], [i]) for i in range(sys_.n)]
+    # the residual is far above the tolerance, and different rows give different norms
+    sc = O.scales(sys_, x_np)
+    bound = Fraction(synth.TOL_P[sys_.K]) * Fraction(float(sc["s_b"].sum())) * sys_.n
+    assert want > 1000 * bound and len(set(others)) > 1
+    assert abs(got - want) <= bound, (float(got), float(want))

@@ -224,6 +224,13 @@ def test_reuse_qr_and_ledger():
     led = h.ledger()
     assert led["steps"] == 2 and led["qr_count"] == 1      # "QR once"
     assert led["ms_convolution"] > 0 and led["ms_stage"] > 0
+    # operation counts beside the times: the closed forms of SURVEY 8(d) d.4
+    from paper_2301_12659_b200 import perfmodel as PM
+    c = PM.algorithmic_counts(sys_.eq_ptr, sys_.mono_ptr, h.nnz, sys_.n, sys_.d)
+    assert led["md_fma_convolution"] == 2 * c["evaldiff"] and led["md_fma_qr"] == c["qr"]
+    assert led["md_fma_stage"] == 2 * c["stage"] and led["md_fma_residual"] == 2 * c["residual"]
+    assert led["flops_per_md_fma"] == PM.mix_flops(PM.MD_FMA_MIX[4])
+    assert led["fp64_flops"] == led["flops_per_md_fma"] * (2 * c["total"] - c["qr"])
     assert P.lib().ns_newton_series_step(h._h, 8, 16, 7, x.data_ptr(), None, 0, None) == 2   # NS_EPREC
     assert P.lib().ns_newton_series_step(h._h, 4, 15, 7, x.data_ptr(), None, 0, None) == 3   # NS_EDIM
 
@@ -296,6 +303,17 @@ def test_C3_full_parity_start():
     non-vacuous at every k."""
     sys_ = synth.build_config("C3")
     x = synth.make_x(sys_, "start", seed=1)
+    F = O.field_for(8)
+    _full_parity(sys_, x, F, out=H.parallel_step(sys_, x, F), nonvacuous=True)
+
+
+@pytest.mark.slow
+def test_C3_full_parity_rough():
+    """configs[2] with every coefficient perturbed ('rough'): the updates
+    A_j dx_{k-j}, j >= 1, are all nonzero, so the bulk right-looking updates
+    and the stage chain are exercised at every k; full oracle, non-vacuous."""
+    sys_ = synth.build_config("C3")
+    x = synth.make_x(sys_, "rough", seed=1)
     F = O.field_for(8)
     _full_parity(sys_, x, F, out=H.parallel_step(sys_, x, F), nonvacuous=True)
 
@@ -488,3 +506,52 @@ def test_C4_sampled_rows_and_a_posteriori_residual():
         for k in (0, 7, d - 1):
             want = H.limbs_to_fraction(x[:, i, k]) + H.limbs_to_fraction(g["dx"][:, k, i])
             assert abs(H.limbs_to_fraction(xn[:, i, k]) - want) <= Fraction(tol) * abs(want)
+
+
+def test_library_row_replication_kernels_bitwise():
+    """The device half of the library's C4 exchange: three simulated ranks
+    (ns_set_partition on three handles, ranges of ns_exchange_plan) pack their
+    rows with ns_pack_rows into one gather buffer (what the grouped
+    ncclBroadcast delivers to every rank), each unpacks the other blocks into
+    its partial arrays: every rank then holds the unsharded eval/diff bitwise."""
+    import paper_2301_12659_b200 as P
+    torch = _torch()
+    sys_ = synth.banded_two_column_system(48, 6, 9, 4, seed=41)
+    x = torch.tensor(synth.make_x(sys_, "rough", seed=42), device="cuda:0")
+    full = _handle(sys_)
+    fb, fA, f0 = full.eval_diff(x)
+    bounds, cnt = P.exchange_plan(sys_.eq_ptr, sys_.mono_ptr, sys_.var_idx, sys_.n, sys_.D, sys_.K, 3)
+    off = np.concatenate([[0], np.cumsum(cnt)])
+    gather = torch.zeros(int(off[-1]), dtype=torch.float64, device="cuda:0")
+    parts = []
+    for r in range(3):
+        h = _handle(sys_)
+        h.set_partition(int(bounds[r]), int(bounds[r + 1]))
+        pb, pA, p0 = h.eval_diff(x)
+        h.pack_rows(int(bounds[r]), int(bounds[r + 1]), pb, pA, p0, gather[off[r]:off[r + 1]])
+        parts.append((h, pb, pA, p0))
+    for r, (h, pb, pA, p0) in enumerate(parts):
+        for q in range(3):
+            if q != r:
+                h.pack_rows(int(bounds[q]), int(bounds[q + 1]), pb, pA, p0, gather[off[q]:off[q + 1]], unpack=True)
+        assert torch.equal(pb, fb) and torch.equal(pA, fA) and torch.equal(p0, f0), r
+
+
+def test_library_nccl_comm_single_rank():
+    """ns_nccl_unique_id + ns_comm_init on one rank (the library-owned NCCL
+    communicator; one GPU here): the step through the sharded path equals the
+    plain step bitwise and the communicator reports no asynchronous error."""
+    import paper_2301_12659_b200 as P
+    torch = _torch()
+    sys_ = synth.banded_two_column_system(40, 6, 9, 4, seed=43)
+    x_np = synth.make_x(sys_, "rough", seed=44)
+    ref = _handle(sys_)
+    xa = torch.tensor(x_np, device="cuda:0")
+    ref.step(xa)
+    h = _handle(sys_)
+    h.comm_init(1, 0, P.nccl_unique_id())
+    xb = torch.tensor(x_np, device="cuda:0")
+    h.step(xb)
+    torch.cuda.synchronize()
+    assert torch.equal(xa, xb)
+    assert h.comm_status() == 0
