@@ -293,6 +293,11 @@ int32_t ns_get_qr_trace(ns_system* sys, int64_t* host, int32_t capacity_steps);
  * stamps of the bulk: the last row of pend_k complete.  host_out holds 5 d
  * values.  Returns d, or -1 without a trace. */
 int32_t ns_get_stage_trace(ns_system* sys, int64_t* host_out);
+/* Phase trace of the last batched step (handle created with env
+ * NS_BATCH_TRACE=1): per CTA, 8 globaltimer stamps (ns) of its first path:
+ * start, eval/diff, QR, tile inverses / M, stage loop, residual + update, -, -.
+ * Synchronises.  Returns the number of CTAs, -1 without a trace. */
+int32_t ns_get_batch_trace(ns_system* sys, int64_t* host, int32_t capacity_ctas);
 /* Synchronises; per-class milliseconds accumulated over steps run with NS_LEDGER. */
 ns_status ns_get_ledger(ns_system* sys, ns_ledger* host_out);
 ns_status ns_reset_ledger(ns_system* sys);

@@ -66,8 +66,39 @@ class MPField:
         return Fraction(m * 2 ** e) if e >= 0 else Fraction(m, 2 ** (-e))
 
 
-def field_for(K: int, exact: bool = False):
-    """O-exact, or O-hp at >= 2x the md bits (256 / 512 / 1024 for 2d / 4d / 8d)."""
+class ComplexMPField(MPField):
+    """Complex scalars (NEXT-2): mpmath mpc at ``prec`` bits in a
+    private context.  abs() is the modulus (pivoting, norms)."""
+    is_complex = True
+
+    def __init__(self, prec: int):
+        super().__init__(prec)
+        self.name = f"mpc{prec}"
+        self.zero = self.ctx.mpc(0)
+        self.one = self.ctx.mpc(1)
+
+    def num(self, f):
+        return self.ctx.mpc(f)
+
+    def from_climbs(self, re_limbs, im_limbs):
+        """exact sums of the dyadic limbs of each component, rounded once"""
+        re = sum((Fraction(float(l)) for l in re_limbs), Fraction(0))
+        im = sum((Fraction(float(l)) for l in im_limbs), Fraction(0))
+        c = self.ctx
+        return c.mpc(c.mpf(re.numerator) / c.mpf(re.denominator), c.mpf(im.numerator) / c.mpf(im.denominator))
+
+    def to_fraction(self, v):
+        """(re, im) as exact Fractions"""
+        re = MPField.to_fraction(self, self.ctx.mpf(v.real))
+        im = MPField.to_fraction(self, self.ctx.mpf(v.imag))
+        return re, im
+
+
+def field_for(K: int, exact: bool = False, complex_: bool = False):
+    """O-exact, or O-hp at >= 2x the md bits (256 / 512 / 1024 for 2d / 4d / 8d);
+    complex_: the complex O-hp field (NEXT-2)."""
+    if complex_:
+        return ComplexMPField({2: 256, 4: 512, 8: 1024}[K])
     if exact:
         return ExactField()
     return MPField({2: 256, 4: 512, 8: 1024}[K])
@@ -108,18 +139,23 @@ def product(series_list, d, F):
 # var_idx, coeff [K][M], rhs [K][n][d])
 # --------------------------------------------------------------------------
 def read_x(x_planes, F):
-    """x float64 [K][n][d] (limb planes) -> list of n series of field scalars."""
+    """x float64 [K][n][d] (limb planes), or [2][K][n][d] for a complex system
+    (real planes, then imaginary) -> list of n series of field scalars."""
+    if x_planes.ndim == 4:
+        _, K, n, d = x_planes.shape
+        return [[F.from_climbs(x_planes[0, :, j, k], x_planes[1, :, j, k]) for k in range(d)] for j in range(n)]
     K, n, d = x_planes.shape
     return [[F.from_limbs(x_planes[:, j, k]) for k in range(d)] for j in range(n)]
 
 
 def read_coeffs(sys, F):
+    if getattr(sys, "is_complex", False):
+        return [F.from_climbs(sys.coeff[0, :, t], sys.coeff[1, :, t]) for t in range(sys.M)]
     return [F.from_limbs(sys.coeff[:, t]) for t in range(sys.M)]
 
 
 def read_rhs(sys, F):
-    K, n, d = sys.rhs.shape
-    return [[F.from_limbs(sys.rhs[:, i, k]) for k in range(d)] for i in range(n)]
+    return read_x(sys.rhs, F)
 
 
 def monomial_vars(sys, t):
@@ -406,6 +442,13 @@ def _absconv(a, b, d):
     return c
 
 
+def _mag(planes):
+    """float64 magnitudes of the leading limbs: |v| of [K][...] planes, the
+    modulus of [2][K][...] complex planes"""
+    return np.hypot(planes[0, 0], planes[1, 0]) if planes.ndim >= 2 and planes.shape[0] == 2 and \
+        planes.ndim == 4 else np.abs(planes[0])
+
+
 def scales(sys, x_planes):
     """Magnitude scales for the tolerance rule ||gpu - oracle|| <= tol_p * s
     (SURVEY.md 8(c) c.4), for the eval/diff outputs:
@@ -416,9 +459,10 @@ def scales(sys, x_planes):
     float64 magnitudes of the leading limbs (they scale errors; they are not
     results)."""
     n, d = sys.n, sys.d
-    xa = np.abs(x_planes[0])                      # [n][d]
-    ra = np.abs(sys.rhs[0])
-    ca = np.abs(sys.coeff[0])
+    cx = getattr(sys, "is_complex", False)
+    xa = _mag(x_planes)                           # [n][d]
+    ra = _mag(sys.rhs)
+    ca = np.hypot(sys.coeff[0, 0], sys.coeff[1, 0]) if cx else np.abs(sys.coeff[0])
     s_b = np.zeros((d, n))
     s_A = {}
     for i in range(n):
@@ -451,7 +495,7 @@ def stage_scales(sys, x_planes, A0_float, dx_float, s_b, s_A):
         SA[:, i, j] = ser
     inv_abs = np.abs(np.linalg.inv(A0_float))
     dxa = np.abs(dx_float)
-    xa = np.abs(x_planes[0]).T                     # [d][n]
+    xa = _mag(x_planes).T                          # [d][n]
     e = np.zeros((d, n))
     s = np.zeros(d)
     for k in range(d):

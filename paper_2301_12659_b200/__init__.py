@@ -38,7 +38,7 @@ EXPORTS = ["ns_system_create", "ns_system_destroy", "ns_newton_series_step",
            "ns_newton_series_step_from", "ns_get_trace", "ns_get_qr_trace", "ns_set_window",
            "ns_get_stage_norms", "ns_run_newton", "ns_get_stage_trace",
            "ns_set_residual_sample", "ns_fabry_ratio", "ns_nccl_unique_id", "ns_comm_init",
-           "ns_exchange_plan", "ns_comm_status", "ns_pack_rows"]
+           "ns_exchange_plan", "ns_comm_status", "ns_pack_rows", "ns_get_batch_trace"]
 
 
 class NSError(RuntimeError):
@@ -111,6 +111,7 @@ def lib() -> ctypes.CDLL:
         "ns_get_trace": ([vp, vp, i32, vp], i32),
         "ns_get_qr_trace": ([vp, vp, i32], i32),
         "ns_get_stage_trace": ([vp, vp], i32),
+        "ns_get_batch_trace": ([vp, vp, i32], i32),
         "ns_set_residual_sample": ([vp, vp, ctypes.c_int], ctypes.c_int),
         "ns_fabry_ratio": ([vp, vp, vp, vp], ctypes.c_int),
         "ns_nccl_unique_id": ([vp], ctypes.c_int),
@@ -371,6 +372,14 @@ class NewtonSystem:
         if int(lib().ns_get_stage_trace(self._h, t.ctypes.data)) < 0:
             raise RuntimeError("no stage trace (create the handle with NS_STAGE_TRACE=1)")
         return t[:4 * self.d].reshape(self.d, 4), t[4 * self.d:]
+
+    def batch_trace(self):
+        """Phase stamps of the last batched step (env NS_BATCH_TRACE=1 at create): [CTAs][8] ns."""
+        t = np.zeros((4096, 8), np.int64)
+        g = int(lib().ns_get_batch_trace(self._h, t.ctypes.data, 4096))
+        if g < 0:
+            raise RuntimeError("no batch trace (create the handle with NS_BATCH_TRACE=1)")
+        return t[:g]
 
     def last_launch_count(self) -> int:
         return int(lib().ns_last_launch_count(self._h))

@@ -140,7 +140,7 @@ void free_all(ns_system* s) {
                   s->coeff, s->rhs, s->b, s->A, s->A0, s->W, s->vhead, s->beta, s->rdiag, s->R, s->Qt,
                   s->invR, s->bp, s->dx, s->y, s->part, s->Minv, s->Z, s->pend, s->sflags, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
                   s->bar, s->status, s->bws, s->A0q, s->qr_flags, s->jobs, s->ser_off, s->pool, s->prog, s->left,
-                  s->left_init, s->trace, s->strace, s->sample_rows, s->bpart};
+                  s->left_init, s->trace, s->strace, s->sample_rows, s->bpart, s->strace_b};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& row : s->ev)
@@ -365,6 +365,11 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->left_init, M) == cudaSuccess;
   if (const char* e = getenv("NS_STAGE_TRACE"))
     if (atoi(e)) ok &= dalloc(&s->strace, (size_t)5 * s->d) == cudaSuccess;
+  if (const char* e = getenv("NS_BATCH_TRACE"))
+    if (atoi(e)) {
+      s->btrace_on = true;
+      ok &= dalloc(&s->strace_b, (size_t)8 * 4 * s->sms * 4) == cudaSuccess;  // up to 16 CTAs per SM
+    }
   if (const char* e = getenv("NS_TRACE"))
     if (atoi(e)) ok &= dalloc(&s->trace, 3 * jobs.size() + 6 * 256) == cudaSuccess;
   if (!ok) return fail(NS_ENOMEM);
@@ -473,6 +478,15 @@ int32_t ns_get_qr_trace(ns_system* s, int64_t* host, int32_t capacity_steps) {
       cudaMemcpy(host, s->cqr_trace, sizeof(long long) * 8 * ns_, cudaMemcpyDeviceToHost) != cudaSuccess)
     return -1;
   return ns_;
+}
+
+int32_t ns_get_batch_trace(ns_system* s, int64_t* host, int32_t capacity_ctas) {
+  if (!s || !s->strace_b || !host) return -1;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  const int g = std::min(capacity_ctas, s->btrace_grid);
+  if (g > 0 && cudaMemcpy(host, s->strace_b, sizeof(long long) * 8 * g, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return g;
 }
 
 int32_t ns_get_stage_trace(ns_system* s, int64_t* host) {

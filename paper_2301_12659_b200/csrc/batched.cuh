@@ -24,7 +24,7 @@ struct BLayout {
 template <int K>
 __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, double* X, const double* RHS,
                                                            double* RES, double* gws_all, BLayout L,
-                                                           int TB) {
+                                                           int TB, long long* trace) {
   extern __shared__ double smem[];
   __shared__ int s_next;
   const int n = s.n, d = s.d, nnz = s.nnz;
@@ -52,7 +52,11 @@ __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, 
   const int T = (n + TB - 1) / TB;
   const long long lsI = (long long)T * TB * TB;
 
+  // phase stamps (globaltimer) of the CTA's first path: start, eval/diff, QR, tiles, stages, residual
+  long long* tr = (trace && tid == 0) ? trace + 8LL * blockIdx.x : nullptr;
   for (int p = blockIdx.x; p < batch; p += gridDim.x) {
+    if (p != (int)blockIdx.x) tr = nullptr;
+    if (tr) tr[0] = gtimer();
     double* x = X + (size_t)p * K * n * d;
     const double* rhs = RHS ? RHS + (size_t)p * K * n * d : s.rhs;
     // identity half of [A0 | I]
@@ -146,6 +150,7 @@ __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, 
       __syncwarp();
     }
     __syncthreads();
+    if (tr) tr[1] = gtimer();
     // ||b_k||_1 of the evaluated b (before the stage loop turns b into b')
     for (int k = warp; k < d; k += NW) {
       md::mdv<K> acc = md::zero<K>();
@@ -160,6 +165,7 @@ __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, 
       for (int c = j + 1 + warp; c < ncol; c += NW) apply_reflector<K, false>(n, j, c, W, vh, be);
       __syncthreads();
     }
+    if (tr) tr[2] = gtimer();
     // ------------------------------------------------ inverses of R's diagonal tiles
     for (int tc = warp; tc < T * TB; tc += NW) {
       const int t = tc / TB, cl = tc % TB, t0 = t * TB;
@@ -187,6 +193,7 @@ __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, 
       }
     }
     __syncthreads();
+    if (tr) tr[3] = gtimer();
     // ------------------------------------------------ stage loop
     for (int k = 0; k < d; ++k) {
       // updates: b'_k,i = b_k,i - sum_{j=1}^{k} sum_e A_j[e] dx_{k-j}[col e]
@@ -239,6 +246,7 @@ __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, 
         __syncthreads();
       }
     }
+    if (tr) tr[4] = gtimer();
     // ------------------------------------------------ residual r_k = b'_k - A_0 dx_k, norms
     for (int k = warp; k < d; k += NW) {
       md::mdv<K> nr = md::zero<K>(), nx = md::zero<K>();
@@ -273,6 +281,7 @@ __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, 
       md::store<K>(RES + (size_t)p * K * 3, 3, lane, best);
     }
     __syncthreads();
+    if (tr) tr[5] = gtimer();
   }
 }
 

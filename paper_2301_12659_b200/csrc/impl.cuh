@@ -366,7 +366,9 @@ ns_status batched_impl(ns_system* s, int batch, double* x, const double* rhs, do
     s->bws_per_path = need;
   }
   DevSys ds = devsys(s);
-  ns::batched_step_kernel<K><<<grid, threads, smem_bytes, st>>>(ds, batch, x, rhs, res, s->bws, L, TB);
+  ns::batched_step_kernel<K><<<grid, threads, smem_bytes, st>>>(ds, batch, x, rhs, res, s->bws, L, TB,
+                                                                  s->btrace_on ? s->strace_b : nullptr);
+  s->btrace_grid = grid;
   s->last_launches = 1;
   s->last_stream = st;
   CK(cudaGetLastError());

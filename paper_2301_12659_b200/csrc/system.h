@@ -83,6 +83,9 @@ struct ns_system {
   double* bws = nullptr;
   size_t bws_per_path = 0;
   size_t batched_smem = 0;
+  bool btrace_on = false;          // NS_BATCH_TRACE=1 at create: phase stamps of the batched kernel
+  long long* strace_b = nullptr;   // [grid][8]
+  int btrace_grid = 0;
 };
 
 

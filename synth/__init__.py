@@ -93,6 +93,7 @@ class System:
     rhs: np.ndarray         # float64 [K][n][d]
     exact: tuple
     meta: dict = field(default_factory=dict)
+    is_complex: bool = False  # NEXT-2: coeff [2][K][M], rhs [2][K][n][d] (real planes, then imaginary)
 
     @property
     def d(self) -> int:
@@ -405,3 +406,83 @@ def build_config(name: str, K: int | None = None, n: int | None = None, D: int |
     if c["kind"] == "band2":
         return banded_two_column_system(n, min(c["w"], n), D, K, seed, name=name)
     raise ValueError(name)
+
+
+# --------------------------------------------------------------------------
+# NEXT-2: complex coefficients
+# --------------------------------------------------------------------------
+def _cmul(a, b):
+    return (a[0] * b[0] - a[1] * b[1], a[0] * b[1] + a[1] * b[0])
+
+
+def unit_circle(count: int, seed: int) -> list[tuple[float, float]]:
+    """count points (cos t, sin t), t ~ U[0, 2 pi) from PCG64(seed), rounded to
+    doubles: "random complex numbers on the unit circle" (P:369-370); the
+    rounded values are the exact inputs (|z| = 1 to within 2^-53)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    th = rng.uniform(0.0, 2.0 * math.pi, size=count)
+    return [(float(math.cos(t)), float(math.sin(t))) for t in th]
+
+
+def _cplanes(values, K, shape):
+    """exact complex values (Fraction pairs) -> planes [2][K][...] rounded limb by limb"""
+    out = np.zeros((2, K) + shape)
+    flat = out.reshape(2, K, -1)
+    for e, (re, im) in enumerate(values):
+        flat[0, :, e] = rational_to_md(re.numerator, re.denominator, K)
+        flat[1, :, e] = rational_to_md(im.numerator, im.denominator, K)
+    return out
+
+
+def complex_triangular_system(n: int, D: int, K: int, seed: int = 0, name: str = "TS1c") -> System:
+    """The triangular system of Eq.(5) with complex data (NEXT-2):
+    equation i is c_i x_0 x_1 ... x_i = r_i(t) with c_i and alpha_j on the unit
+    circle; exact solution x_j = exp(alpha_j t), so r_i =
+    c_i exp(S_i t), S_i = sum_{j<=i} alpha_j, coefficients c_i S_i^k / k! (exact
+    Gaussian rationals, rounded limb by limb per component)."""
+    from fractions import Fraction as Fr
+    eqs = [[list(range(i + 1))] for i in range(n)]
+    eq_ptr, mono_ptr, var_idx = _csr(eqs)
+    alphas = unit_circle(n, seed)
+    cs = unit_circle(n, seed + 104729)
+    d = D + 1
+    rhs_vals = []
+    for i in range(n):
+        S = (sum(Fr(alphas[j][0]) for j in range(i + 1)), sum(Fr(alphas[j][1]) for j in range(i + 1)))
+        c = (Fr(cs[i][0]), Fr(cs[i][1]))
+        p = c
+        row = []
+        for k in range(d):
+            row.append((p[0] / math.factorial(k), p[1] / math.factorial(k)))
+            p = _cmul(p, S)
+        rhs_vals.append(row)
+    rhs = _cplanes([v for row in rhs_vals for v in row], K, (n, d))
+    coeff = _cplanes([(Fr(c[0]), Fr(c[1])) for c in cs], K, (n,))
+    return System(name, n, D, K, eq_ptr, mono_ptr, var_idx, coeff, rhs, ("cexp", alphas), {"seed": seed},
+                  is_complex=True)
+
+
+def make_cx(system: System, kind: str = "near", seed: int = 1) -> np.ndarray:
+    """Complex starting series [2][K][n][d] (reading R11 per component): 'exact'
+    the rounded exp(alpha t); 'start' x_0 (1 + u h), higher coefficients 0;
+    'near' / 'rough' every coefficient times (1 + u h), h = HALF_PREC[K] /
+    2^-12, u ~ U[-1, 1] real from PCG64(seed)."""
+    from fractions import Fraction as Fr
+    n, d, K = system.n, system.d, system.K
+    rng = np.random.Generator(np.random.PCG64(seed))
+    u = rng.uniform(-1.0, 1.0, size=(n, d))
+    h = Fr(1, 2 ** 12) if kind == "rough" else Fr(HALF_PREC[K])
+    vals = []
+    for j in range(n):
+        a = (Fr(system.exact[1][j][0]), Fr(system.exact[1][j][1]))
+        p = (Fr(1), Fr(0))
+        for k in range(d):
+            v = (p[0] / math.factorial(k), p[1] / math.factorial(k))
+            if kind == "start" and k > 0:
+                v = (Fr(0), Fr(0))
+            elif kind != "exact":
+                f = 1 + Fr(float(u[j, k])) * h
+                v = (v[0] * f, v[1] * f)
+            vals.append(v)
+            p = _cmul(p, a)
+    return _cplanes(vals, K, (n, d))

@@ -578,3 +578,92 @@ def test_step_window_x0_factor():
     A1dx = O.matvec_sparse(mod["A"], 1, mod["dx"][0], 2, FX)
     r0, r1 = b[0][1] - A1dx[0], b[1][1] - A1dx[1]
     assert mod["dx"][1] == [r0, (r1 - 3 * r0) / 2]
+
+
+# ---------------------------------------------------------------- NEXT-2: complex coefficients
+def test_complex_generator_unit_circle_and_exact_rhs():
+    """alpha_j and c_i on the unit circle (within 2^-52); the rhs is
+    c_i S_i^k / k! exactly rounded per component (Gaussian rationals)."""
+    sys_ = synth.complex_triangular_system(4, 5, 4, seed=3)
+    for a in sys_.exact[1]:
+        assert abs(a[0] ** 2 + a[1] ** 2 - 1.0) < 2.0 ** -50
+    al = [complex(*a) for a in sys_.exact[1]]
+    F = O.field_for(4, complex_=True)
+    rhs = O.read_rhs(sys_, F)
+    co = O.read_coeffs(sys_, F)
+    for i in range(4):
+        S = F.ctx.mpc(0)
+        for j in range(i + 1):
+            S += F.ctx.mpc(*sys_.exact[1][j])
+        for k in range(6):
+            want = co[i] * S ** k / F.ctx.factorial(k)
+            assert abs(rhs[i][k] - want) <= F.ctx.mpf(2) ** -205 * (1 + abs(want))
+    assert abs(abs(al[0]) - 1) < 1e-15
+
+
+def test_complex_monomial_value_and_partials_closed_form():
+    """At x_j = exp(alpha_j t), complex alpha on the unit circle: a monomial is
+    exp(S t) and d/dx_j of it exp((S - alpha_j) t) (SURVEY c.5 closed form,
+    the 4M products of P:630-648 computed by the oracle's truncated
+    convolutions of complex series)."""
+    F = O.ComplexMPField(800)
+    al = synth.unit_circle(6, 9)
+    d = 9
+    x = [[F.ctx.mpc(*a) ** k / F.ctx.factorial(k) for k in range(d)] for a in al]
+    vs = [0, 2, 3, 5]
+    S = sum((F.ctx.mpc(*al[v]) for v in vs), F.ctx.mpc(0))
+    tol = F.ctx.mpf(2) ** -700
+    got = O.monomial_value(x, vs, d, F)
+    for k in range(d):
+        assert abs(got[k] - S ** k / F.ctx.factorial(k)) < tol
+    for j in vs:
+        Sj = S - F.ctx.mpc(*al[j])
+        p = O.monomial_partial(x, vs, j, d, F)
+        for k in range(d):
+            assert abs(p[k] - Sj ** k / F.ctx.factorial(k)) < tol
+
+
+def test_complex_solve_vs_numpy_dense_block_system():
+    """Eq.(4) over C: the oracle's block forward substitution (complex LU with
+    modulus pivoting) against numpy's complex dense solve of the (nd)x(nd)
+    block system."""
+    sys_ = synth.complex_triangular_system(4, 3, 2, seed=5)
+    x = synth.make_cx(sys_, "rough", seed=6)
+    F = O.field_for(2, complex_=True)
+    b, A = O.evaluate(sys_, O.read_x(x, F), F)
+    n, d = 4, 4
+    dx = O.solve(A, b, n, d, F)
+    M = np.zeros((n * d, n * d), complex)
+    rhs = np.zeros(n * d, complex)
+    for k in range(d):
+        for kk in range(k + 1):
+            for i, row in A.items():
+                for c, ser in row.items():
+                    M[k * n + i, kk * n + c] = complex(ser[k - kk])
+        for i in range(n):
+            rhs[k * n + i] = complex(b[i][k])
+    sol = np.linalg.solve(M, rhs)
+    got = np.array([complex(dx[k][i]) for k in range(d) for i in range(n)])
+    assert np.allclose(got, sol, rtol=1e-9, atol=1e-12)
+    r = O.residual(A, b, dx, n, d, F)
+    assert max(abs(v) for rk in r for v in rk) < F.ctx.mpf(2) ** -200
+
+
+def test_complex_newton_converges_and_fixed_point():
+    """Quadratic convergence over C (SURVEY c.3) to exp(alpha t), alpha on the
+    unit circle: coefficients k <= 2^i - 2 exact to the working precision after
+    i steps; at the exact solution the update is ~0."""
+    F = O.ComplexMPField(600)
+    sys_ = synth.complex_triangular_system(4, 6, 8, seed=7)
+    n, d = sys_.n, sys_.d
+    ex = O.read_x(synth.make_cx(sys_, "exact"), F)
+    xs = O.read_x(synth.make_cx(sys_, "start", seed=8), F)
+    for it in range(1, 5):
+        b, A = O.evaluate(sys_, xs, F)
+        dx = O.solve(A, b, n, d, F)
+        xs = [[xs[j][k] + dx[k][j] for k in range(d)] for j in range(n)]
+        for k in range(min(2 ** it - 1, d)):
+            assert max(abs(xs[j][k] - ex[j][k]) for j in range(n)) < F.ctx.mpf(2) ** -380, (it, k)
+    b, A = O.evaluate(sys_, ex, F)
+    dx = O.solve(A, b, n, d, F)
+    assert max(abs(v) for dk in dx for v in dk) < F.ctx.mpf(2) ** -400
