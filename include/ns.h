@@ -81,8 +81,15 @@ typedef struct {
   const int32_t* eq_ptr;   /* host [dim+1]: monomials of eq i = [eq_ptr[i], eq_ptr[i+1])  */
   const int32_t* mono_ptr; /* host [M+1]: variables of monomial t = var_idx[mono_ptr[t]..] */
   const int32_t* var_idx;  /* host: strictly increasing per monomial, < dim (exponent 1)  */
-  const double* coeff;     /* host [K][M] md coefficient c_t; NULL = all ones             */
-  const double* rhs;       /* host [K][dim][D+1] right-hand side series r_i(t)            */
+  const double* coeff;     /* host [C][K][M] md coefficient c_t; NULL = all ones          */
+  const double* rhs;       /* host [C][K][dim][D+1] right-hand side series r_i(t)         */
+  int32_t is_complex;      /* 0: real (C = 1); 1: complex coefficients and series (NEXT-2,
+                              P:630-655), C = 2 component planes, real then imaginary:
+                              component c, limb l of element e at base[(c K + l) plane + e].
+                              A complex handle runs the batched kernel (4M products,
+                              complex Householder): ns_newton_series_step (batch 1) and
+                              ns_newton_series_step_batched; every other entry point
+                              returns NS_EINVAL for it                                   */
 } ns_system_desc;
 
 typedef struct {
@@ -143,9 +150,12 @@ ns_status ns_newton_series_step(ns_system* sys, int precision, int dim, int degr
                                 double* residual_out, uint32_t flags, void* stream);
 
 /* Same step for `batch` independent paths of the same monomial structure
- * (SURVEY 8(e) C5).  x_series: device [batch][K][dim][degree+1];
- * rhs: device [batch][K][dim][degree+1] or NULL (= the handle's rhs for every
- * path); residual_out: device [batch][K][3] or NULL.  batch <= max_batch. */
+ * (SURVEY 8(e) C5), one CTA per path (batched.cuh).  x_series: device
+ * [batch][C][K][dim][degree+1]; rhs: device [batch][C][K][dim][degree+1] or
+ * NULL (= the handle's rhs for every path); residual_out: device
+ * [batch][K][3] (real md norms) or NULL.  batch <= max_batch; the layout,
+ * grid and workspace were sized at create (no allocation here).  flags: 0
+ * (the residual is always formed: NS_EINVAL for any flag). */
 ns_status ns_newton_series_step_batched(ns_system* sys, int precision, int dim, int degree, int batch,
                                         double* x_series, const double* rhs, double* residual_out,
                                         uint32_t flags, void* stream);

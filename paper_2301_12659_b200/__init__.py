@@ -51,7 +51,7 @@ class _Desc(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int32), ("degree", ctypes.c_int32), ("precision", ctypes.c_int32),
                 ("n_monomials", ctypes.c_int32), ("max_batch", ctypes.c_int32),
                 ("eq_ptr", ctypes.c_void_p), ("mono_ptr", ctypes.c_void_p), ("var_idx", ctypes.c_void_p),
-                ("coeff", ctypes.c_void_p), ("rhs", ctypes.c_void_p)]
+                ("coeff", ctypes.c_void_p), ("rhs", ctypes.c_void_p), ("is_complex", ctypes.c_int32)]
 
 
 class StepInfo(ctypes.Structure):
@@ -184,7 +184,7 @@ class NewtonSystem:
     """
 
     def __init__(self, eq_ptr, mono_ptr, var_idx, coeff, rhs, dim: int, degree: int, precision: int,
-                 max_batch: int = 1, device: int = 0):
+                 max_batch: int = 1, device: int = 0, is_complex: bool = False):
         L = lib()
         self._keep = [np.ascontiguousarray(eq_ptr, np.int32), np.ascontiguousarray(mono_ptr, np.int32),
                       np.ascontiguousarray(var_idx, np.int32),
@@ -193,19 +193,22 @@ class NewtonSystem:
         e, m, v, c, r = self._keep
         desc = _Desc(dim, degree, precision, len(m) - 1, max_batch,
                      e.ctypes.data, m.ctypes.data, v.ctypes.data,
-                     None if c is None else c.ctypes.data, r.ctypes.data)
+                     None if c is None else c.ctypes.data, r.ctypes.data, 1 if is_complex else 0)
         h = ctypes.c_void_p()
         _check(L.ns_system_create(ctypes.byref(desc), device, ctypes.byref(h)), "ns_system_create")
         self._h = h
         self.n, self.D, self.K, self.max_batch, self.device = dim, degree, precision, max_batch, device
         self.d = degree + 1
+        self.C = 2 if is_complex else 1
+        self._xshape = ((2,) if is_complex else ()) + (precision, dim, degree + 1)
         self.nnz = int(L.ns_nnz(h))
 
     @classmethod
     def from_system(cls, sysobj, max_batch: int = 1, device: int = 0):
         """Build from a synth.System-like object (duck typed)."""
         return cls(sysobj.eq_ptr, sysobj.mono_ptr, sysobj.var_idx, sysobj.coeff, sysobj.rhs,
-                   sysobj.n, sysobj.D, sysobj.K, max_batch=max_batch, device=device)
+                   sysobj.n, sysobj.D, sysobj.K, max_batch=max_batch, device=device,
+                   is_complex=getattr(sysobj, "is_complex", False))
 
     def close(self):
         if getattr(self, "_h", None):
@@ -220,8 +223,8 @@ class NewtonSystem:
 
     # ---- the hot path
     def step(self, x, residual_out=None, flags: int = 0, stream=None):
-        """ns_newton_series_step: x [K][n][d] CUDA float64, updated in place."""
-        _require_cuda(x, "x", (self.K, self.n, self.d))
+        """ns_newton_series_step: x [K][n][d] ([2][K][n][d] complex) CUDA float64, updated in place."""
+        _require_cuda(x, "x", self._xshape)
         if residual_out is not None:
             _require_cuda(residual_out, "residual_out", (self.K, 3))
         _check(lib().ns_newton_series_step(self._h, self.K, self.n, self.D, _ptr(x), _ptr(residual_out),
@@ -230,9 +233,9 @@ class NewtonSystem:
     def step_batched(self, x, rhs=None, residual_out=None, flags: int = 0, stream=None):
         """ns_newton_series_step_batched: x [B][K][n][d]."""
         B = x.shape[0]
-        _require_cuda(x, "x", (B, self.K, self.n, self.d))
+        _require_cuda(x, "x", (B,) + self._xshape)
         if rhs is not None:
-            _require_cuda(rhs, "rhs", (B, self.K, self.n, self.d))
+            _require_cuda(rhs, "rhs", (B,) + self._xshape)
         if residual_out is not None:
             _require_cuda(residual_out, "residual_out", (B, self.K, 3))
         _check(lib().ns_newton_series_step_batched(self._h, self.K, self.n, self.D, B, _ptr(x), _ptr(rhs),

@@ -239,8 +239,10 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
       if (q > a && desc->var_idx[q] <= desc->var_idx[q - 1]) return NS_EMONO;
     }
   }
+  if (desc->is_complex != 0 && desc->is_complex != 1) return NS_EINVAL;
   ns_system* s = new (std::nothrow) ns_system();
   if (!s) return NS_ENOMEM;
+  s->is_complex = desc->is_complex == 1;
   s->dev = cuda_device;
   s->n = n;
   s->D = D;
@@ -314,8 +316,9 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->row_ptr, n + 1) == cudaSuccess;
   ok &= dalloc(&s->col_idx, s->nnz) == cudaSuccess;
   ok &= dalloc(&s->job_order, n) == cudaSuccess;
-  ok &= dalloc(&s->coeff, (size_t)K * M) == cudaSuccess;
-  ok &= dalloc(&s->rhs, (size_t)K * n * d) == cudaSuccess;
+  const size_t Cc = s->is_complex ? 2 : 1;
+  ok &= dalloc(&s->coeff, Cc * K * M) == cudaSuccess;
+  ok &= dalloc(&s->rhs, Cc * K * n * d) == cudaSuccess;
   ok &= dalloc(&s->b, (size_t)K * d * n) == cudaSuccess;
   ok &= dalloc(&s->A, (size_t)K * d * s->nnz) == cudaSuccess;
   ok &= dalloc(&s->A0, (size_t)K * nn) == cudaSuccess;
@@ -351,9 +354,9 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->status, 1) == cudaSuccess;
   if (!ok) return fail(NS_ENOMEM);
   switch (K) {
-    case 2: st = Impl<2>::setup(s); break;
-    case 4: st = Impl<4>::setup(s); break;
-    default: st = Impl<8>::setup(s); break;
+    case 2: st = Impl<2>::setup(s); if (!st) st = Impl<2>::batched_setup(s); break;
+    case 4: st = Impl<4>::setup(s); if (!st) st = Impl<4>::batched_setup(s); break;
+    default: st = Impl<8>::setup(s); if (!st) st = Impl<8>::batched_setup(s); break;
   }
   if (st) return fail(st);
   ok = true;
@@ -378,8 +381,8 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= cudaMemcpy(s->left_init, left.data(), sizeof(int) * M, cudaMemcpyHostToDevice) == cudaSuccess;
   if (!ok) return fail(NS_ECUDA);
   // upload
-  std::vector<double> coeff((size_t)K * M, 0.0);
-  if (desc->coeff) std::memcpy(coeff.data(), desc->coeff, sizeof(double) * K * M);
+  std::vector<double> coeff(Cc * K * M, 0.0);
+  if (desc->coeff) std::memcpy(coeff.data(), desc->coeff, sizeof(double) * Cc * K * M);
   else
     for (int t = 0; t < M; ++t) coeff[t] = 1.0;
   ok = true;
@@ -390,8 +393,8 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= cudaMemcpy(s->row_ptr, s->h_row_ptr.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice) == cudaSuccess;
   ok &= cudaMemcpy(s->col_idx, s->h_col_idx.data(), sizeof(int) * s->nnz, cudaMemcpyHostToDevice) == cudaSuccess;
   ok &= cudaMemcpy(s->job_order, s->h_job_order.data(), sizeof(int) * n, cudaMemcpyHostToDevice) == cudaSuccess;
-  ok &= cudaMemcpy(s->coeff, coeff.data(), sizeof(double) * K * M, cudaMemcpyHostToDevice) == cudaSuccess;
-  ok &= cudaMemcpy(s->rhs, desc->rhs, sizeof(double) * K * n * d, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(s->coeff, coeff.data(), sizeof(double) * Cc * K * M, cudaMemcpyHostToDevice) == cudaSuccess;
+  ok &= cudaMemcpy(s->rhs, desc->rhs, sizeof(double) * Cc * K * n * d, cudaMemcpyHostToDevice) == cudaSuccess;
   ok &= cudaMemset(s->status, 0, sizeof(unsigned)) == cudaSuccess;
   ok &= cudaMemset(s->bar, 0, 8 * sizeof(unsigned)) == cudaSuccess;
   for (auto& row : s->ev)
@@ -419,6 +422,15 @@ ns_status ns_newton_series_step(ns_system* s, int precision, int dim, int degree
   if (!s || !x) return NS_EINVAL;
   if (precision != s->K) return NS_EPREC;
   if (dim != s->n || degree != s->D) return NS_EDIM;
+  if (s->is_complex) {  // NEXT-2: the batched kernel on one path (include/ns.h)
+    if (flags) return NS_EINVAL;
+    if (s->k_lo != 0 || s->dc != s->d) return NS_ESTATE;
+    switch (s->K) {
+      case 2: return Impl<2>::batched(s, 1, x, nullptr, res_out, 0, (cudaStream_t)stream);
+      case 4: return Impl<4>::batched(s, 1, x, nullptr, res_out, 0, (cudaStream_t)stream);
+      default: return Impl<8>::batched(s, 1, x, nullptr, res_out, 0, (cudaStream_t)stream);
+    }
+  }
   if (flags & ~(NS_REUSE_QR | NS_NO_RESIDUAL | NS_LEDGER | NS_TILED_BS)) return NS_EINVAL;
   if ((flags & NS_REUSE_QR) && !s->qr_cached) return NS_ESTATE;
   // M = R^{-1} Q^T (~n^3/2 md-FMA once per QR) saves 2T barriers per stage.
@@ -438,7 +450,7 @@ ns_status ns_newton_series_step_batched(ns_system* s, int precision, int dim, in
   if (!s || !x) return NS_EINVAL;
   if (precision != s->K) return NS_EPREC;
   if (dim != s->n || degree != s->D || batch < 0 || batch > s->max_batch) return NS_EDIM;
-  if (flags & ~(NS_NO_RESIDUAL)) return NS_EINVAL;
+  if (flags) return NS_EINVAL;
   if (s->k_lo != 0 || s->dc != s->d) return NS_ESTATE;  // the batched kernel runs the full window
   if (batch == 0) return NS_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -451,6 +463,7 @@ ns_status ns_newton_series_step_batched(ns_system* s, int precision, int dim, in
 
 ns_status ns_eval_diff(ns_system* s, const double* x, double* b, double* A, double* A0, void* stream) {
   if (!s || !x) return NS_EINVAL;
+  if (s->is_complex) return NS_EINVAL;  // complex: the batched kernel path only (include/ns.h)
   cudaStream_t st = (cudaStream_t)stream;
   ns_status r;
   s->last_launches = 0;
@@ -522,6 +535,7 @@ int32_t ns_get_trace(ns_system* s, int64_t* host, int32_t capacity_jobs, int32_t
 
 ns_status ns_set_partition(ns_system* s, int eq_lo, int eq_hi) {
   if (!s || eq_lo < 0 || eq_hi > s->n || eq_lo >= eq_hi) return NS_EINVAL;
+  if (s->is_complex) return NS_EINVAL;  // complex: the batched kernel path only (include/ns.h)
   std::vector<int4> jobs;
   std::vector<long long> ser_off;
   std::vector<int> left;
@@ -540,6 +554,7 @@ ns_status ns_newton_series_step_from(ns_system* s, int precision, int dim, int d
                                      const double* A, const double* A0, double* res_out, uint32_t flags,
                                      void* stream) {
   if (!s || !x || !b || !A || !A0) return NS_EINVAL;
+  if (s->is_complex) return NS_EINVAL;  // complex: the batched kernel path only (include/ns.h)
   if (precision != s->K) return NS_EPREC;
   if (dim != s->n || degree != s->D) return NS_EDIM;
   if (flags & ~(NS_REUSE_QR | NS_NO_RESIDUAL | NS_LEDGER | NS_TILED_BS)) return NS_EINVAL;
@@ -576,6 +591,7 @@ ns_status ns_newton_series_step_from(ns_system* s, int precision, int dim, int d
 
 ns_status ns_set_window(ns_system* s, int k_lo, int dc) {
   if (!s || k_lo < 0 || dc > s->d || k_lo >= dc) return NS_EINVAL;
+  if (s->is_complex) return NS_EINVAL;  // complex: the batched kernel path only (include/ns.h)
   s->k_lo = k_lo;
   s->dc = dc;
   return NS_OK;
@@ -583,6 +599,7 @@ ns_status ns_set_window(ns_system* s, int k_lo, int dc) {
 
 ns_status ns_set_residual_sample(ns_system* s, const int32_t* rows, int count) {
   if (!s || count < 0 || count > s->n || (count > 0 && !rows)) return NS_EINVAL;
+  if (s->is_complex) return NS_EINVAL;  // complex: the batched kernel path only (include/ns.h)
   if (count == 0) {
     s->n_sample = 0;
     return NS_OK;
@@ -603,6 +620,7 @@ ns_status ns_set_residual_sample(ns_system* s, const int32_t* rows, int count) {
 
 ns_status ns_fabry_ratio(ns_system* s, const double* x, double* z, void* stream) {
   if (!s || !x || !z || s->d < 2) return NS_EINVAL;
+  if (s->is_complex) return NS_EINVAL;  // complex: the batched kernel path only (include/ns.h)
   cudaStream_t st = (cudaStream_t)stream;
   switch (s->K) {
     case 2: return Impl<2>::fabry(s, x, z, st);
@@ -626,6 +644,7 @@ ns_status ns_get_stage_norms(ns_system* s, double* out) {
 ns_status ns_run_newton(ns_system* s, int precision, int dim, int degree, double* x, int max_iter, double eps,
                         uint32_t flags, void* stream, ns_iter_log* log, ns_run_info* info) {
   if (!s || !x || max_iter < 0) return NS_EINVAL;
+  if (s->is_complex) return NS_EINVAL;  // complex: the batched kernel path only (include/ns.h)
   if (precision != s->K) return NS_EPREC;
   if (dim != s->n || degree != s->D) return NS_EDIM;
   if (flags & ~(NS_QR_ONCE | NS_NO_STAGGER | NS_LEDGER | NS_TILED_BS | NS_NO_RESIDUAL)) return NS_EINVAL;
@@ -715,6 +734,7 @@ ns_status ns_jacobian_pattern(const ns_system* s, int32_t* row_ptr, int32_t* col
 ns_status ns_toeplitz_solve(ns_system* s, const double* b, const double* A, const double* A0, double* dx,
                             void* stream) {
   if (!s || !b || !A || !A0 || !dx) return NS_EINVAL;
+  if (s->is_complex) return NS_EINVAL;  // complex: the batched kernel path only (include/ns.h)
   cudaStream_t st = (cudaStream_t)stream;
   const size_t K = s->K, d = s->d, n = s->n;
   CK(cudaMemcpyAsync(s->b, b, sizeof(double) * K * d * n, cudaMemcpyDeviceToDevice, st));

@@ -1,74 +1,151 @@
-// batched.cuh -- the whole Newton step for a batch of independent paths of the
-// same monomial structure, one CTA per path (persistent), every step of
-// SURVEY 8(a) a1-a11 inside the CTA (independent units, no
-// collective).  Warps evaluate/differentiate equations (warp-level
-// convolutions, same reverse-mode job list as evaldiff.cuh); the QR of [A_0|I],
-// the tile inversion and the stage loop use the CTA's shared memory.
+// batched.cuh -- the whole Newton step for a batch of
+// independent paths of one monomial structure, one CTA per path (persistent;
+// independent units, no collective), real or complex scalars
+// (scalar.cuh; NEXT-2).
+//
+// Per path, inside the CTA (arrays in shared memory when the layout fits,
+// else in the CTA's slice of the global workspace, BLayout):
+//   eval/diff   warp per equation (LPT order), reverse mode of Eq.(12): the
+//               forward and backward chains of a monomial advance together,
+//               the cross products run as one batch; every convolution output
+//               pair (k, d-1-k) is summed by ONE lane (d+1 terms, no padding,
+//               no butterfly), the accumulation in unnormalised level sums
+//               renormalised once per output.  b_i = r_i - sum c x^tau and the
+//               A row in ascending monomial order (reading R20).
+//   QR          Householder on [A_0 | I]: a group of TPC lanes owns a
+//               column (rows dealt round robin), reflector j by the group of
+//               column j, then every other column group applies it; after n
+//               steps W = [R | Q^H].  Complex: alpha = -(x_0/|x_0|) ||x||,
+//               beta = 1 / (||x|| (||x|| + |x_0|)) (reading R13 generalised).
+//   tiles       inverses of the TB x TB diagonal tiles of R (recursive doubling)
+//   stages      for k = 0..D: y = Q^H b'_k, tiled back substitution
+//               R dx_k = y, then right-looking updates
+//               b'_{k'} -= A_{k'-k} dx_k for every k' > k (the updates of
+//               P:680-689 applied as soon as dx_k exists; per (k', i) the
+//               contributions k = 0, 1, ... arrive in order: deterministic)
+//   residual    r_k = b'_k - A_0 dx_k, norms, x += dx.
+// Only __syncthreads between phases; no grid-wide synchronisation.
 #pragma once
 #include "evaldiff.cuh"
-#include "solve.cuh"
+#include "scalar.cuh"
+#include "system.h"
 
 namespace ns {
 
-// Byte offsets of the per-path arrays; each lives in shared memory when its
-// `in_smem` bit is set, else in the CTA's global workspace slice.
-struct BLayout {
-  size_t off_W, off_invR, off_b, off_dx, off_y, off_vh, off_beta, off_kn;  // doubles
-  unsigned in_smem;  // bit i for the arrays in the order above
-  size_t smem_doubles;
-  size_t gws_doubles;   // per CTA: A + per-warp series + arrays not in smem
-  size_t off_A_g;       // in gws
-  size_t off_ser_g;     // per-warp F/G/X series block in gws
+// BLayout and the array ids B_* are in system.h (the host sizes the layout)
+
+template <class A>
+MD_INL void acc_select(A& dst, const A& x, const A& y, bool take_x) {
+  constexpr int N = sizeof(A) / sizeof(double);
+  double* o = reinterpret_cast<double*>(&dst);
+  const double* a = reinterpret_cast<const double*>(&x);
+  const double* b = reinterpret_cast<const double*>(&y);
+#pragma unroll
+  for (int i = 0; i < N; ++i) o[i] = take_x ? a[i] : b[i];
+}
+
+struct BSer {
+  const double* p;  // coefficient 0 of limb plane 0 of component 0
+  long long ls;     // limb-plane stride
 };
 
-template <int K>
+// B truncated convolutions out_b = a_b * b_b (b < B) on one warp: lane per
+// output pair (k1, k2 = d-1-k1), both sums in one loop of d+1 terms (k1 + 1
+// terms of c_{k1}, then k2 + 1 of c_{k2}) with the accumulator chosen per
+// term (no divergence), outputs compact series (limb stride ldo).
+template <class S, typename Get>
+__device__ void sconv_warp(int lane, int B, int d, int ldo, Get get) {
+  using V = typename S::V;
+  using Acc = typename S::Acc;
+  const int P = (d + 1) / 2;
+  for (int g0 = 0; g0 < B * P; g0 += 32) {
+    const int gid = g0 + lane;
+    if (gid < B * P) {
+      const int bi = gid / P, p = gid % P;
+      const int k1 = p, k2 = d - 1 - p;
+      const int tot = (k1 == k2) ? k1 + 1 : d + 1;
+      BSer a, b;
+      double* out;
+      get(bi, a, b, out);
+      Acc a1, a2;
+      S::acc_zero(a1);
+      S::acc_zero(a2);
+      for (int t = 0; t < tot; ++t) {
+        const bool first = t <= k1;
+        const int k = first ? k1 : k2;
+        const int j = first ? t : t - k1 - 1;
+        const V xa = S::load(a.p, a.ls, j), yb = S::load(b.p, b.ls, k - j);
+        Acc cur;
+        acc_select(cur, a1, a2, first);
+        S::acc_prod(cur, xa, yb);
+        acc_select(a1, cur, a1, first);
+        acc_select(a2, a2, cur, first);
+      }
+      S::store(out, ldo, k1, S::val(a1));
+      if (k2 != k1) S::store(out, ldo, k2, S::val(a2));
+    }
+  }
+}
+
+template <class S, int K>
 __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, double* X, const double* RHS,
                                                            double* RES, double* gws_all, BLayout L,
-                                                           int TB, long long* trace) {
+                                                           long long* trace) {
+  using V = typename S::V;
+  using R = typename S::R;
+  using Acc = typename S::Acc;
+  constexpr int C = S::C;
   extern __shared__ double smem[];
   __shared__ int s_next;
   const int n = s.n, d = s.d, nnz = s.nnz;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NW = blockDim.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x;
   double* gws = gws_all + (size_t)blockIdx.x * L.gws_doubles;
-  auto P = [&](int bit, size_t off) -> double* {
-    return ((L.in_smem >> bit) & 1u) ? (smem + off) : (gws + off);
-  };
-  double* W = P(0, L.off_W);
-  double* invR = P(1, L.off_invR);
-  double* bb = P(2, L.off_b);    // b, then b' in place  [K][d][n]
-  double* dxv = P(3, L.off_dx);  // [K][d][n]
-  double* yv = P(4, L.off_y);    // [K][n]
-  double* vh = P(5, L.off_vh);
-  double* be = P(6, L.off_beta);
-  double* kn = P(7, L.off_kn);   // [3][K][d]
-  double* A = gws + L.off_A_g;   // [K][d][nnz]
-  const long long ser = (long long)K * d;
+  auto Pa = [&](int a) -> double* { return ((L.in_smem >> a) & 1u) ? (smem + L.off[a]) : (gws + L.off[a]); };
+  double* xs = Pa(B_X);    // x    [C][K][n][d]
+  double* bb = Pa(B_B);    // b -> pending b' -> r  [C][K][d][n]
+  double* dxv = Pa(B_DX);  // dx   [C][K][d][n]
+  double* W = Pa(B_W);     // [A_0 | I] -> [R | Q^H], column major [C][K][2n][n]
+  double* RI = Pa(B_RI);   // inverted diagonal tiles of R [C][K][T][TB][TB]
+  double* yv = Pa(B_Y);    // y = Q^H b'_k, scratch of the tile inverses [C][K][max(n, TB^2/2)]
+  double* vh = Pa(B_VH);   // v_0 of each reflector [C][K][n]
+  double* be = Pa(B_BE);   // beta of each reflector (real) [K][n]
+  double* kn = Pa(B_KN);   // per-k norms (real) [3][K][d]: b, r, dx
+  double* A = gws + L.off_A_g;  // [C][K][d][nnz]
+  const long long lsX = (long long)n * d, lsV = (long long)d * n, lsW = 2LL * n * n, lsA = (long long)d * nnz;
+  const int TB = L.TB, T = (n + TB - 1) / TB, TT = TB * TB;
+  const long long lsI = (long long)T * TT;
+  const long long lsY = (long long)max(n, TT / 2);
+  const long long ser = (long long)C * K * d;  // one compact series
   double* Fw = gws + L.off_ser_g + (size_t)warp * 3 * s.m_max * ser;
   double* Gw = Fw + s.m_max * ser;
   double* Xw = Gw + s.m_max * ser;
   const int ncol = 2 * n;
-  const long long lsW = (long long)ncol * n, lsV = (long long)d * n, lsA = (long long)d * nnz;
-  const long long lsX = (long long)n * d;
-  const int T = (n + TB - 1) / TB;
-  const long long lsI = (long long)T * TB * TB;
-
-  // phase stamps (globaltimer) of the CTA's first path: start, eval/diff, QR, tiles, stages, residual
+  int TPC = 1;  // lanes per column of the QR (power of two <= 32, ncol TPC <= NT)
+  while (TPC < 32 && ncol * TPC * 2 <= NT) TPC <<= 1;
+  int TPO = 1;  // lanes per output of the Q^H and tile matvecs
+  while (TPO < 32 && n * TPO * 2 <= NT) TPO <<= 1;
   long long* tr = (trace && tid == 0) ? trace + 8LL * blockIdx.x : nullptr;
+
   for (int p = blockIdx.x; p < batch; p += gridDim.x) {
     if (p != (int)blockIdx.x) tr = nullptr;
     if (tr) tr[0] = gtimer();
-    double* x = X + (size_t)p * K * n * d;
-    const double* rhs = RHS ? RHS + (size_t)p * K * n * d : s.rhs;
-    // identity half of [A0 | I]
-    for (long long t = tid; t < (long long)K * n * n; t += blockDim.x) {
+    double* xg = X + (size_t)p * C * K * n * d;
+    const double* rhs = RHS ? RHS + (size_t)p * C * K * n * d : s.rhs;
+    // ---------------------------------------------------- inputs: x, b = r, I half of W
+    for (int t = tid; t < C * K * n * d; t += NT) {
+      xs[t] = xg[t];
+      const int ck = t / (n * d), r = t % (n * d), i = r / d, k = r % d;
+      bb[(long long)ck * lsV + (long long)k * n + i] = rhs[t];
+    }
+    for (long long t = tid; t < (long long)C * K * n * n; t += NT) {
       const int r = (int)(t % n);
       const long long lc = t / n;
-      const int c = (int)(lc % n), l = (int)(lc / n);
-      W[(long long)l * lsW + (long long)(n + c) * n + r] = (l == 0 && r == c) ? 1.0 : 0.0;
+      const int c = (int)(lc % n), ck = (int)(lc / n);
+      W[(long long)ck * lsW + (long long)(n + c) * n + r] = (ck == 0 && r == c) ? 1.0 : 0.0;
     }
     if (tid == 0) s_next = 0;
     __syncthreads();
-    // ------------------------------------------------ eval/diff, warp per equation
+    // ---------------------------------------------------- eval/diff, warp per equation
     for (;;) {
       int job = 0;
       if (lane == 0) job = atomicAdd(&s_next, 1);
@@ -76,207 +153,258 @@ __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, 
       if (job >= n) break;
       const int i = s.job_order[job];
       const int r0 = s.row_ptr[i], len = s.row_ptr[i + 1] - r0;
-      for (int t = lane; t < K * d; t += 32) {
-        const int l = t / d, k = t % d;
-        bb[(long long)l * lsV + (long long)k * n + i] = rhs[(long long)l * lsX + (long long)i * d + k];
-      }
-      for (int t = lane; t < K * d * len; t += 32) A[(long long)(t / len) * nnz + r0 + t % len] = 0.0;
+      for (int t = lane; t < C * K * d * len; t += 32) A[(long long)(t / len) * nnz + r0 + t % len] = 0.0;
       __syncwarp();
       for (int tau = s.eq_ptr[i]; tau < s.eq_ptr[i + 1]; ++tau) {
         const int m0 = s.mono_ptr[tau];
         const int m = s.mono_ptr[tau + 1] - m0;
         const int* vars = s.var_idx + m0;
         const int* dst = s.mono_dst + m0;
-        md::mdv<K> c;
-#pragma unroll
-        for (int l = 0; l < K; ++l) c.x[l] = s.coeff[(long long)l * s.M + tau];
+        const V c = S::load(s.coeff, s.M, tau);
+        auto xser = [&](int v) { return BSer{xs + (long long)v * d, lsX}; };
         if (m >= 2) {
+          // layer q: f_q = f_{q-1} * x_{v(q+1)} and g_q = g_{q-1} * x_{v(m-q)} (Eq.(12))
           for (int q = 1; q <= m - 1; ++q) {
             const int nb = (q <= m - 2) ? 2 : 1;
-            conv_batch<K>(lane, 32, nb, d, [&](int bi, SerRef& pa, SerRef& pb, double*& pc) {
+            sconv_warp<S>(lane, nb, d, d, [&](int bi, BSer& pa, BSer& pb, double*& pc) {
               if (bi == 0) {
-                pa = (q == 1) ? SerRef{x + (long long)vars[0] * d, lsX} : SerRef{Fw + (q - 1) * ser, d};
-                pb = SerRef{x + (long long)vars[q] * d, lsX};
+                pa = (q == 1) ? xser(vars[0]) : BSer{Fw + (q - 1) * ser, d};
+                pb = xser(vars[q]);
                 pc = Fw + q * ser;
               } else {
-                pa = (q == 1) ? SerRef{x + (long long)vars[m - 1] * d, lsX} : SerRef{Gw + (q - 1) * ser, d};
-                pb = SerRef{x + (long long)vars[m - 1 - q] * d, lsX};
+                pa = (q == 1) ? xser(vars[m - 1]) : BSer{Gw + (q - 1) * ser, d};
+                pb = xser(vars[m - 1 - q]);
                 pc = Gw + q * ser;
               }
             });
             __syncwarp();
           }
-          if (m >= 3) {
-            conv_batch<K>(lane, 32, m - 2, d, [&](int bi, SerRef& pa, SerRef& pb, double*& pc) {
-              const int j = bi + 2;  // 1-based variable position
-              pa = (j - 2 == 0) ? SerRef{x + (long long)vars[0] * d, lsX} : SerRef{Fw + (j - 2) * ser, d};
+          if (m >= 3) {  // cross products d/dx_{v_j} = f_{j-2} * g_{m-j-1}, j = 2..m-1 (Eq.(13))
+            sconv_warp<S>(lane, m - 2, d, d, [&](int bi, BSer& pa, BSer& pb, double*& pc) {
+              const int j = bi + 2;
+              pa = (j - 2 == 0) ? xser(vars[0]) : BSer{Fw + (j - 2) * ser, d};
               const int gq = m - j - 1;
-              pb = (gq == 0) ? SerRef{x + (long long)vars[m - 1] * d, lsX} : SerRef{Gw + gq * ser, d};
+              pb = (gq == 0) ? xser(vars[m - 1]) : BSer{Gw + gq * ser, d};
               pc = Xw + (j - 1) * ser;
             });
             __syncwarp();
           }
         }
-        for (int k = lane; k < d; k += 32) {
-          md::mdv<K> val = (m == 1) ? md::load<K>(x + (long long)vars[0] * d, lsX, k)
-                                    : md::load<K>(Fw + (m - 1) * ser, d, k);
-          md::mdv<K> acc = md::load<K>(bb + (long long)k * n, lsV, i);
-          md::store<K>(bb + (long long)k * n, lsV, i, md::fma_acc<K>(acc, md::neg<K>(c), val));
+        for (int k = lane; k < d; k += 32) {  // b_i -= c x^tau
+          const V val = (m == 1) ? S::load(xs + (long long)vars[0] * d, lsX, k) : S::load(Fw + (m - 1) * ser, d, k);
+          S::store(bb + (long long)k * n, lsV, i, S::fma(S::load(bb + (long long)k * n, lsV, i), S::neg(c), val));
         }
-        for (int t = lane; t < m * d; t += 32) {
+        for (int t = lane; t < m * d; t += 32) {  // A[i][v_q] += c d x^tau / d x_{v_q}
           const int q = t % m, k = t / m;
-          md::mdv<K> part;
-          if (m == 1) part = md::from_double<K>(k == 0 ? 1.0 : 0.0);
-          else if (m == 2) part = md::load<K>(x + (long long)vars[1 - q] * d, lsX, k);
-          else if (q == 0) part = md::load<K>(Gw + (m - 2) * ser, d, k);
-          else if (q == m - 1) part = md::load<K>(Fw + (m - 2) * ser, d, k);
-          else part = md::load<K>(Xw + q * ser, d, k);
+          V part;
+          if (m == 1) part = (k == 0) ? S::one() : S::zero();
+          else if (m == 2) part = S::load(xs + (long long)vars[1 - q] * d, lsX, k);
+          else if (q == 0) part = S::load(Gw + (m - 2) * ser, d, k);
+          else if (q == m - 1) part = S::load(Fw + (m - 2) * ser, d, k);
+          else part = S::load(Xw + q * ser, d, k);
           const long long e = dst[q];
-          md::mdv<K> acc = md::load<K>(A + (long long)k * nnz, lsA, e);
-          md::store<K>(A + (long long)k * nnz, lsA, e, md::fma_acc<K>(acc, c, part));
+          S::store(A + (long long)k * nnz, lsA, e, S::fma(S::load(A + (long long)k * nnz, lsA, e), c, part));
         }
         __syncwarp();
       }
-      // dense row i of A0 into W (column-major): W[j][i]
-      for (int t = lane; t < K * n; t += 32) {
-        const int l = t / n, j = t % n;
-        W[(long long)l * lsW + (long long)j * n + i] = 0.0;
-      }
+      // dense row i of A_0 into W (column major: W[j][i])
+      for (int t = lane; t < C * K * n; t += 32) W[(long long)(t / n) * lsW + (long long)(t % n) * n + i] = 0.0;
       __syncwarp();
-      for (int t = lane; t < K * len; t += 32) {
-        const int l = t / len, e = r0 + t % len;
-        W[(long long)l * lsW + (long long)s.col_idx[e] * n + i] = A[(long long)l * lsA + e];
+      for (int t = lane; t < C * K * len; t += 32) {
+        const int ck = t / len, e = r0 + t % len;
+        W[(long long)ck * lsW + (long long)s.col_idx[e] * n + i] = A[(long long)ck * lsA + e];
       }
       __syncwarp();
     }
     __syncthreads();
     if (tr) tr[1] = gtimer();
-    // ||b_k||_1 of the evaluated b (before the stage loop turns b into b')
-    for (int k = warp; k < d; k += NW) {
-      md::mdv<K> acc = md::zero<K>();
-      for (int i = lane; i < n; i += 32) acc = md::add<K>(acc, md::absv<K>(md::load<K>(bb + (long long)k * n, lsV, i)));
+    // ||b_k|| of the evaluated b (before the stage loop turns b into b')
+    for (int k = warp; k < d; k += NT / 32) {
+      R acc = md::zero<K>();
+      for (int i = lane; i < n; i += 32) acc = md::add<K>(acc, S::absv(S::load(bb + (long long)k * n, lsV, i)));
       acc = md::group_sum<K>(acc, 32);
       if (lane == 0) md::store<K>(kn, d, k, acc);
     }
-    // ------------------------------------------------ Householder QR of [A0 | I]
-    for (int j = 0; j < n; ++j) {
-      if (warp == 0) make_reflector<K, false>(n, j, W, vh, be, nullptr, nullptr);
-      __syncthreads();
-      for (int c = j + 1 + warp; c < ncol; c += NW) apply_reflector<K, false>(n, j, c, W, vh, be);
-      __syncthreads();
-    }
-    if (tr) tr[2] = gtimer();
-    // ------------------------------------------------ inverses of R's diagonal tiles
-    for (int tc = warp; tc < T * TB; tc += NW) {
-      const int t = tc / TB, cl = tc % TB, t0 = t * TB;
-      const int nb = min(TB, n - t0);
-      md::mdv<K> inv_d = md::zero<K>();
-      if (lane < nb) {
-        md::mdv<K> rqq = md::load<K>(W, lsW, (long long)(t0 + lane) * n + t0 + lane);
-        inv_d = md::recip<K>(rqq);
-      }
-      md::mdv<K> Xc = md::zero<K>();
-      if (cl < nb) {
-        if (lane == cl) Xc = inv_d;
-        for (int r = cl - 1; r >= 0; --r) {
-          md::mdv<K> pr = md::zero<K>();
-          if (lane > r && lane <= cl)
-            pr = md::mul<K>(md::load<K>(W, lsW, (long long)(t0 + lane) * n + t0 + r), Xc);
-          pr = md::group_sum<K>(pr, 32);
-          md::mdv<K> xr = md::neg<K>(md::mul<K>(pr, md::shfl<K>(inv_d, r)));
-          if (lane == r) Xc = xr;
-        }
-      }
-      if (lane < TB) {
-        md::mdv<K> v = (lane < nb && cl < nb && lane <= cl) ? Xc : md::zero<K>();
-        md::store<K>(invR, lsI, (long long)t * TB * TB + (long long)lane * TB + cl, v);
-      }
-    }
-    __syncthreads();
-    if (tr) tr[3] = gtimer();
-    // ------------------------------------------------ stage loop
-    for (int k = 0; k < d; ++k) {
-      // updates: b'_k,i = b_k,i - sum_{j=1}^{k} sum_e A_j[e] dx_{k-j}[col e]
-      if (k > 0) {
-        for (int i = warp; i < n; i += NW) {
-          const int r0 = s.row_ptr[i], len = s.row_ptr[i + 1] - r0;
-          md::mdv<K> acc = md::zero<K>();
-          for (int t = lane; t < k * len; t += 32) {
-            const int j = 1 + t / len, e = r0 + t % len;
-            acc = md::fma_acc<K>(acc, md::load<K>(A + (long long)j * nnz, lsA, e),
-                                 md::load<K>(dxv + (long long)(k - j) * n, lsV, s.col_idx[e]));
-          }
-          acc = md::group_sum<K>(acc, 32);
+    // ---------------------------------------------------- Householder QR of [A_0 | I]
+    {
+      const int sub = tid % TPC;
+      const int slots = (ncol + NT / TPC - 1) / (NT / TPC);  // column slots per lane group (uniform)
+      for (int j = 0; j < n; ++j) {
+        // reflector j by warp 0
+        if (warp == 0) {
+          Acc sg;
+          S::acc_zero(sg);
+          for (int r = j + lane; r < n; r += 32) S::acc_abs2(sg, S::load(W, lsW, (long long)j * n + r));
+          S::acc_group(sg, 32);
+          const R sig = S::rval(sg);
+          const V x0 = S::load(W, lsW, (long long)j * n + j);
+          const R nrm = md::sqrt<K>(sig);
+          const R ax0 = S::absv(x0);
+          const V alpha = S::neg(S::mul_real(S::phase(x0, ax0), nrm));
+          const V v0 = S::sub(x0, alpha);
+          R bt = md::zero<K>();
+          if (!md::is_zero<K>(sig)) bt = md::recip<K>(md::mul<K>(nrm, md::add<K>(nrm, ax0)));
           if (lane == 0) {
-            md::mdv<K> bk = md::load<K>(bb + (long long)k * n, lsV, i);
-            md::store<K>(bb + (long long)k * n, lsV, i, md::sub<K>(bk, acc));
+            S::store(vh, n, j, v0);
+            md::store<K>(be, n, j, bt);
+            S::store(W, lsW, (long long)j * n + j, alpha);
+          }
+        }
+        __syncthreads();
+        const V v0 = S::load(vh, n, j);
+        const R bt = md::load<K>(be, n, j);
+        for (int sl = 0; sl < slots; ++sl) {
+          // every lane takes part in the group shuffles (idle groups sum nothing)
+          const int cg = sl * (NT / TPC) + tid / TPC;
+          const bool act = cg < ncol && cg > j;
+          Acc dt;
+          S::acc_zero(dt);
+          for (int r = j + sub; act && r < n; r += TPC) {
+            const V v = (r == j) ? v0 : S::load(W, lsW, (long long)j * n + r);
+            S::acc_prod(dt, S::conj(v), S::load(W, lsW, (long long)cg * n + r));
+          }
+          S::acc_group(dt, TPC);
+          const V nw = S::neg(S::mul_real(S::val(dt), bt));
+          for (int r = j + sub; act && r < n; r += TPC) {
+            const V v = (r == j) ? v0 : S::load(W, lsW, (long long)j * n + r);
+            const long long e = (long long)cg * n + r;
+            S::store(W, lsW, e, S::fma(S::load(W, lsW, e), nw, v));
           }
         }
         __syncthreads();
       }
-      // qhb: y_r = sum_c (Q^T)[r][c] b'_k[c], Q^T in W columns n..2n-1 (thread per row)
-      for (int r = tid; r < n; r += blockDim.x) {
-        md::mdv<K> acc = md::zero<K>();
-        for (int c = 0; c < n; ++c)
-          acc = md::fma_acc<K>(acc, md::load<K>(W, lsW, (long long)(n + c) * n + r),
-                               md::load<K>(bb + (long long)k * n, lsV, c));
-        md::store<K>(yv, n, r, acc);
+    }
+    if (tr) tr[2] = gtimer();
+    // ---------------------------------------------------- inverses of R's diagonal tiles
+    // inv([[A, B], [0, C]]) = [[inv A, -inv A B inv C], [0, inv C]] by doubling
+    // sizes 2, 4, .., TB; R[r][c] = W[c][r]; scratch T1 in yv
+    for (int t = 0; t < T; ++t) {
+      const int t0 = t * TB, nb = min(TB, n - t0);
+      double* Xt = RI + (long long)t * TT;
+      for (int e = tid; e < TT; e += NT) {
+        const int r = e / TB, c = e % TB;
+        V v = S::zero();
+        if (r == c) v = (r < nb) ? S::recip(S::load(W, lsW, (long long)(t0 + r) * n + t0 + r)) : S::one();
+        S::store(Xt, lsI, e, v);
       }
       __syncthreads();
-      // bs by tiles, last to first
+      for (int sz = 2; sz <= TB; sz <<= 1) {
+        const int h = sz >> 1, nent = (TB / sz) * h * h;
+        // T1[blk][p][q] = sum_{u=0}^{q} R[base+p][base+h+u] X[base+h+u][base+h+q]
+        for (int e = tid; e < nent; e += NT) {
+          const int blk = e / (h * h), pp = (e / h) % h, q = e % h, base = blk * sz;
+          Acc a;
+          S::acc_zero(a);
+          for (int u = 0; u <= q; ++u) {
+            const int rr = base + pp, cc = base + h + u;
+            const V rv = (rr < nb && cc < nb) ? S::load(W, lsW, (long long)(t0 + cc) * n + t0 + rr) : S::zero();
+            S::acc_prod(a, rv, S::load(Xt, lsI, (long long)cc * TB + base + h + q));
+          }
+          S::store(yv, lsY, e, S::val(a));
+        }
+        __syncthreads();
+        // X[base+p][base+h+q] = - sum_{v=p}^{h-1} X[base+p][base+v] T1[blk][v][q]
+        for (int e = tid; e < nent; e += NT) {
+          const int blk = e / (h * h), pp = (e / h) % h, q = e % h, base = blk * sz;
+          Acc a;
+          S::acc_zero(a);
+          for (int v = pp; v < h; ++v)
+            S::acc_prod(a, S::load(Xt, lsI, (long long)(base + pp) * TB + base + v),
+                        S::load(yv, lsY, (long long)blk * h * h + v * h + q));
+          S::store(Xt, lsI, (long long)(base + pp) * TB + base + h + q, S::neg(S::val(a)));
+        }
+        __syncthreads();
+      }
+    }
+    if (tr) tr[3] = gtimer();
+    // ---------------------------------------------------- stage loop
+    for (int k = 0; k < d; ++k) {
+      // y = Q^H b'_k: (Q^H)[r][c] = W[n + c][r]
+      for (int o0 = 0; o0 < n; o0 += NT / TPO) {  // uniform trip count: every lane joins the shuffles
+        const int o = o0 + tid / TPO, sub = tid % TPO;
+        const bool act = o < n;
+        Acc a;
+        S::acc_zero(a);
+        for (int c = sub; act && c < n; c += TPO)
+          S::acc_prod(a, S::load(W, lsW, (long long)(n + c) * n + o), S::load(bb + (long long)k * n, lsV, c));
+        S::acc_group(a, TPO);
+        if (act && sub == 0) S::store(yv, lsY, o, S::val(a));
+      }
+      __syncthreads();
+      // R dx_k = y by tiles, last to first
       for (int t = T - 1; t >= 0; --t) {
         const int t0 = t * TB, t1 = min(n, t0 + TB);
-        if (t < T - 1) {
-          for (int r = t0 + tid; r < t1; r += blockDim.x) {
-            md::mdv<K> acc = md::zero<K>();
-            for (int c = t1; c < n; ++c)
-              acc = md::fma_acc<K>(acc, md::load<K>(W, lsW, (long long)c * n + r),
-                                   md::load<K>(dxv + (long long)k * n, lsV, c));
-            md::store<K>(yv, n, r, md::sub<K>(md::load<K>(yv, n, r), acc));
+        if (t < T - 1) {  // z = y - R[tile][> t1] dx_k[> t1]  (z kept in y)
+          for (int o0 = t0; o0 < t1; o0 += NT / TPO) {
+            const int o = o0 + tid / TPO, sub = tid % TPO;
+            const bool act = o < t1;
+            Acc a;
+            S::acc_zero(a);
+            for (int c = t1 + sub; act && c < n; c += TPO)
+              S::acc_prod(a, S::load(W, lsW, (long long)c * n + o), S::load(dxv + (long long)k * n, lsV, c));
+            S::acc_group(a, TPO);
+            if (act && sub == 0) S::store(yv, lsY, o, S::sub(S::load(yv, lsY, o), S::val(a)));
           }
           __syncthreads();
         }
-        for (int r = t0 + tid; r < t1; r += blockDim.x) {
-          md::mdv<K> acc = md::zero<K>();
-          for (int c = t0; c < t1; ++c)
-            acc = md::fma_acc<K>(acc, md::load<K>(invR, lsI, (long long)t * TB * TB + (long long)(r - t0) * TB + (c - t0)),
-                                 md::load<K>(yv, n, c));
-          md::store<K>(dxv + (long long)k * n, lsV, r, acc);
+        for (int o0 = t0; o0 < t1; o0 += NT / TPO) {
+          const int o = o0 + tid / TPO, sub = tid % TPO;
+          const bool act = o < t1;
+          Acc a;
+          S::acc_zero(a);
+          for (int c = t0 + sub; act && c < t1; c += TPO)
+            S::acc_prod(a, S::load(RI + (long long)t * TT, lsI, (long long)(o - t0) * TB + (c - t0)),
+                        S::load(yv, lsY, c));
+          S::acc_group(a, TPO);
+          if (act && sub == 0) S::store(dxv + (long long)k * n, lsV, o, S::val(a));
         }
         __syncthreads();
       }
+      // right-looking updates b'_{k'} -= A_{k'-k} dx_k, k' = k+1..D
+      const int npairs = (d - 1 - k) * n;
+      for (int pr = tid; pr < npairs; pr += NT) {
+        const int kp = k + 1 + pr / n, i = pr % n;
+        const int e0 = s.row_ptr[i], e1 = s.row_ptr[i + 1];
+        Acc a;
+        S::acc_zero(a);
+        for (int e = e0; e < e1; ++e)
+          S::acc_prod(a, S::load(A + (long long)(kp - k) * nnz, lsA, e),
+                      S::load(dxv + (long long)k * n, lsV, s.col_idx[e]));
+        const long long o = (long long)kp * n + i;
+        S::store(bb, lsV, o, S::sub(S::load(bb, lsV, o), S::val(a)));
+      }
+      __syncthreads();
     }
     if (tr) tr[4] = gtimer();
-    // ------------------------------------------------ residual r_k = b'_k - A_0 dx_k, norms
-    for (int k = warp; k < d; k += NW) {
-      md::mdv<K> nr = md::zero<K>(), nx = md::zero<K>();
-      for (int i = lane; i < n; i += 32) {
-        const int r0 = s.row_ptr[i], r1 = s.row_ptr[i + 1];
-        md::mdv<K> acc = md::zero<K>();
-        for (int e = r0; e < r1; ++e)
-          acc = md::fma_acc<K>(acc, md::load<K>(A, lsA, e), md::load<K>(dxv + (long long)k * n, lsV, s.col_idx[e]));
-        md::mdv<K> bpk = md::load<K>(bb + (long long)k * n, lsV, i);
-        nr = md::add<K>(nr, md::absv<K>(md::sub<K>(bpk, acc)));
-        nx = md::add<K>(nx, md::absv<K>(md::load<K>(dxv + (long long)k * n, lsV, i)));
-      }
-      nr = md::group_sum<K>(nr, 32);
-      nx = md::group_sum<K>(nx, 32);
-      if (lane == 0) {
-        md::store<K>(kn + (long long)K * d, d, k, nr);
-        md::store<K>(kn + 2LL * K * d, d, k, nx);
-      }
+    // ---------------------------------------------------- residual r_k = b'_k - A_0 dx_k (into bb), norms
+    for (int pr = tid; pr < d * n; pr += NT) {
+      const int k = pr / n, i = pr % n;
+      Acc a;
+      S::acc_zero(a);
+      for (int e = s.row_ptr[i]; e < s.row_ptr[i + 1]; ++e)
+        S::acc_prod(a, S::load(A, lsA, e), S::load(dxv + (long long)k * n, lsV, s.col_idx[e]));
+      S::store(bb, lsV, pr, S::sub(S::load(bb, lsV, pr), S::val(a)));
     }
     __syncthreads();
-    // x += dx
-    for (int t = tid; t < n * d; t += blockDim.x) {
-      const int j = t / d, k = t % d;
-      md::store<K>(x, lsX, t, md::add<K>(md::load<K>(x, lsX, t), md::load<K>(dxv + (long long)k * n, lsV, j)));
+    for (int kw = warp; kw < 2 * d; kw += NT / 32) {
+      const int k = kw % d, w = 1 + kw / d;  // w = 1: r, 2: dx
+      const double* src = (w == 1) ? bb : dxv;
+      R acc = md::zero<K>();
+      for (int i = lane; i < n; i += 32) acc = md::add<K>(acc, S::absv(S::load(src + (long long)k * n, lsV, i)));
+      acc = md::group_sum<K>(acc, 32);
+      if (lane == 0) md::store<K>(kn + (long long)w * K * d, d, k, acc);
     }
+    // x += dx
+    for (int t = tid; t < n * d; t += NT) {
+      const int j = t / d, k = t % d;
+      S::store(xg, lsX, t, S::add(S::load(xs, lsX, t), S::load(dxv + (long long)k * n, lsV, j)));
+    }
+    __syncthreads();
     if (RES && warp == 0 && lane < 3) {
-      md::mdv<K> best = md::zero<K>();
+      R best = md::zero<K>();
       for (int k = 0; k < d; ++k) {
-        md::mdv<K> v = md::load<K>(kn + (long long)lane * K * d, d, k);
-        if (md::greater<K>(v, best)) best = v;
+        const R v = md::load<K>(kn + (long long)lane * K * d, d, k);
+        if (md::greater<K>(v, best) || !isfinite(v.x[0])) best = v;
       }
       md::store<K>(RES + (size_t)p * K * 3, 3, lane, best);
     }

@@ -256,7 +256,7 @@ ns_status ns_pack_rows(const ns_system* s, int lo, int hi, double* b, double* A,
 }
 
 ns_status ns_comm_init(ns_system* s, int nranks, int rank, const void* uid128) {
-  if (!s || nranks < 1 || rank < 0 || rank >= nranks || nranks > s->n || !uid128) return NS_EINVAL;
+  if (!s || nranks < 1 || rank < 0 || rank >= nranks || nranks > s->n || !uid128 || s->is_complex) return NS_EINVAL;
   if (s->k_lo != 0 || s->dc != s->d) return NS_ESTATE;
   NcclApi& N = nccl();
   if (!N.ok) return NS_ENCCL;

@@ -317,57 +317,93 @@ ns_status setup_grids(ns_system* s) {
 }  // namespace
 namespace {
 
-template <int K>
-ns_status batched_impl(ns_system* s, int batch, double* x, const double* rhs, double* res, uint32_t flags,
-                       cudaStream_t st) {
-  (void)flags;
-  const int n = s->n, d = s->d, TB = 32, T = (n + TB - 1) / TB;
-  const int threads = 256, NW = threads / 32;
+// Layout of the batched kernel for this handle (per CTA = per path in
+// flight): the small, hot arrays first into shared memory, as long as the
+// budget allows `ctas` CTAs per SM; the rest, the structural Jacobian A and
+// the per-warp chain series in the CTA's slice of a global workspace.
+template <class S, int K>
+ns::BLayout batched_layout(const ns_system* s, size_t smem_cap_doubles, int threads) {
+  constexpr int C = S::C;
+  const size_t n = s->n, d = s->d, NW = threads / 32;
   ns::BLayout L{};
-  // arrays in order: W, invR, b, dx, y, vhead, beta, knorm
-  const size_t sz[8] = {(size_t)K * 2 * n * n, (size_t)K * T * TB * TB, (size_t)K * d * n, (size_t)K * d * n,
-                        (size_t)K * n, (size_t)K * n, (size_t)K * n, (size_t)3 * K * d};
-  size_t* offs[8] = {&L.off_W, &L.off_invR, &L.off_b, &L.off_dx, &L.off_y, &L.off_vh, &L.off_beta, &L.off_kn};
-  const size_t smem_cap = 200 * 1024 / sizeof(double);  // leave room for static smem
-  // greedy: smallest, hottest arrays first into shared memory
-  const int order[8] = {4, 5, 6, 7, 2, 3, 1, 0};
+  int TB = 1;
+  while (TB * 2 <= std::min<int>(32, s->n)) TB *= 2;
+  L.TB = TB;
+  const size_t T = (n + TB - 1) / TB, TT = (size_t)TB * TB;
+  size_t sz[ns::B_NARR];
+  sz[ns::B_X] = C * K * n * d;
+  sz[ns::B_B] = C * K * d * n;
+  sz[ns::B_DX] = C * K * d * n;
+  sz[ns::B_W] = C * K * 2 * n * n;
+  sz[ns::B_RI] = C * K * T * TT;
+  sz[ns::B_Y] = C * K * std::max(n, TT / 2);
+  sz[ns::B_VH] = C * K * n;
+  sz[ns::B_BE] = K * n;
+  sz[ns::B_KN] = 3 * K * d;
+  const int order[ns::B_NARR] = {ns::B_VH, ns::B_BE, ns::B_KN, ns::B_Y, ns::B_X, ns::B_B, ns::B_DX, ns::B_RI, ns::B_W};
   size_t sm = 0;
-  size_t g = (size_t)K * d * s->nnz + (size_t)NW * 3 * s->m_max * K * d;  // A + warp series
+  size_t g = (size_t)C * K * d * s->nnz + NW * 3 * (size_t)s->m_max * C * K * d;
   L.off_A_g = 0;
-  L.off_ser_g = (size_t)K * d * s->nnz;
+  L.off_ser_g = (size_t)C * K * d * s->nnz;
   L.in_smem = 0;
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < ns::B_NARR; ++q) {
     const int a = order[q];
-    if (sm + sz[a] <= smem_cap) {
-      *offs[a] = sm;
+    if (sm + sz[a] <= smem_cap_doubles) {
+      L.off[a] = sm;
       sm += sz[a];
       L.in_smem |= 1u << a;
     } else {
-      *offs[a] = g;
+      L.off[a] = g;
       g += sz[a];
     }
   }
   L.smem_doubles = sm;
   L.gws_doubles = g;
-  const size_t smem_bytes = sm * sizeof(double);
-  if (cudaFuncSetAttribute(ns::batched_step_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return L;
+}
+
+template <class S, int K>
+ns_status batched_setup_t(ns_system* s) {
+  const int threads = 256;
+  int optin = 0;
+  CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->dev));
+  int per_sm = 0;
+  CK(cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, s->dev));
+  // shared-memory budget per CTA: as many CTAs per SM as the layout allows
+  // (NS_BATCH_CTAS overrides the target), each CTA's static smem and the
+  // per-block reservation (1 KiB) set aside
+  int target = 2;
+  if (const char* e = getenv("NS_BATCH_CTAS")) target = std::max(1, atoi(e));
+  const size_t cap = std::min<size_t>((size_t)optin, (size_t)per_sm / target - 2048) / sizeof(double);
+  ns::BLayout L = batched_layout<S, K>(s, cap, threads);
+  const size_t smem_bytes = L.smem_doubles * sizeof(double);
+  if (cudaFuncSetAttribute(ns::batched_step_kernel<S, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem_bytes) != cudaSuccess)
     return NS_ECUDA;
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::batched_step_kernel<K>, threads, smem_bytes));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::batched_step_kernel<S, K>, threads, smem_bytes));
   if (occ < 1) return NS_ECUDA;
-  const int grid = std::min(batch, occ * s->sms);
-  const size_t need = (size_t)grid * g;
-  if (need > s->bws_per_path) {  // bws_per_path holds the allocated size in doubles
-    if (s->bws) cudaFree(s->bws);
-    s->bws = nullptr;
-    s->bws_per_path = 0;
-    if (dalloc(&s->bws, need) != cudaSuccess) return NS_ENOMEM;
-    s->bws_per_path = need;
-  }
+  s->bl = L;
+  s->b_threads = threads;
+  s->batched_smem = smem_bytes;
+  s->b_grid = std::min(std::max(1, s->max_batch), occ * s->sms);
+  if (dalloc(&s->bws, (size_t)s->b_grid * L.gws_doubles) != cudaSuccess) return NS_ENOMEM;
+  return NS_OK;
+}
+
+template <int K>
+ns_status batched_impl(ns_system* s, int batch, double* x, const double* rhs, double* res, uint32_t flags,
+                       cudaStream_t st) {
+  (void)flags;
   DevSys ds = devsys(s);
-  ns::batched_step_kernel<K><<<grid, threads, smem_bytes, st>>>(ds, batch, x, rhs, res, s->bws, L, TB,
-                                                                  s->btrace_on ? s->strace_b : nullptr);
+  const int grid = std::min(batch, s->b_grid);
+  long long* tr = s->btrace_on ? s->strace_b : nullptr;
+  if (s->is_complex)
+    ns::batched_step_kernel<ns::CplxS<K>, K><<<grid, s->b_threads, s->batched_smem, st>>>(ds, batch, x, rhs, res,
+                                                                                           s->bws, s->bl, tr);
+  else
+    ns::batched_step_kernel<ns::RealS<K>, K><<<grid, s->b_threads, s->batched_smem, st>>>(ds, batch, x, rhs, res,
+                                                                                           s->bws, s->bl, tr);
   s->btrace_grid = grid;
   s->last_launches = 1;
   s->last_stream = st;
@@ -466,6 +502,10 @@ template <int K>
 ns_status Impl<K>::batched(ns_system* s, int batch, double* x, const double* rhs, double* res, uint32_t flags,
                            cudaStream_t st) {
   return batched_impl<K>(s, batch, x, rhs, res, flags, st);
+}
+template <int K>
+ns_status Impl<K>::batched_setup(ns_system* s) {
+  return s->is_complex ? batched_setup_t<ns::CplxS<K>, K>(s) : batched_setup_t<ns::RealS<K>, K>(s);
 }
 template <int K>
 ns_status Impl<K>::md_op(int op, int n, const double* a, const double* b, double* c, cudaStream_t st) {

@@ -8,6 +8,20 @@
 
 struct ns_comm;  // comm.cu
 
+namespace ns {
+// per-path arrays of the batched kernel (batched.cuh): BLayout.off / in_smem bit order
+enum BArr : int { B_X = 0, B_B, B_DX, B_W, B_RI, B_Y, B_VH, B_BE, B_KN, B_NARR };
+struct BLayout {
+  size_t off[B_NARR];   // doubles, in shared memory (bit set) or in the CTA's global slice
+  unsigned in_smem;
+  size_t smem_doubles;  // per CTA
+  size_t gws_doubles;   // per CTA: A + per-warp series + arrays not in shared memory
+  size_t off_A_g;       // A [C][K][d][nnz] in the global slice
+  size_t off_ser_g;     // per-warp F/G/X series blocks in the global slice
+  int TB;               // diagonal tile of R (power of two <= min(32, n))
+};
+}  // namespace ns
+
 struct ns_system {
   int dev = 0;
   int n = 0, D = 0, d = 0, K = 0, M = 0, nnz = 0, m_max = 0, max_batch = 1;
@@ -79,9 +93,11 @@ struct ns_system {
   int last_launches = 0;
   long long series_products = 0, scale_terms = 0;  // S = sum (3m-5), M + sum m (ledger counts)
   ns_comm* comm = nullptr;     // ns_comm_init (comm.cu), nullptr: one GPU
-  // batched
+  // batched (layout, grid and workspace fixed at create: no allocation in a step)
+  bool is_complex = false;         // NEXT-2: complex coefficients (batched kernel path)
   double* bws = nullptr;
-  size_t bws_per_path = 0;
+  ns::BLayout bl{};
+  int b_grid = 0, b_threads = 256;
   size_t batched_smem = 0;
   bool btrace_on = false;          // NS_BATCH_TRACE=1 at create: phase stamps of the batched kernel
   long long* strace_b = nullptr;   // [grid][8]
@@ -111,6 +127,7 @@ struct Impl {
   static ns_status fabry(ns_system* s, const double* x, double* z, cudaStream_t st);
   static ns_status batched(ns_system* s, int batch, double* x, const double* rhs, double* res,
                            uint32_t flags, cudaStream_t st);
+  static ns_status batched_setup(ns_system* s);  // layout, grid, workspace of the batched kernel
   static ns_status md_op(int op, int n, const double* a, const double* b, double* c, cudaStream_t st);
   static ns_status latency(int op, int iters, double* cycles_per_op);
 };

@@ -132,17 +132,34 @@ def _procs():
 
 
 def _pk(v):
-    """field value -> picklable (mpf of a private context does not pickle)"""
+    """field value -> picklable (mpf/mpc of a private context do not pickle)"""
+    if hasattr(v, "_mpc_"):
+        return ("c", v._mpc_)
     return v._mpf_ if hasattr(v, "_mpf_") else v
 
 
 def _unpk(F, t):
+    if isinstance(t, tuple) and len(t) == 2 and t[0] == "c":
+        return F.ctx.make_mpc(t[1])
     return F.ctx.make_mpf(t) if hasattr(F, "ctx") else t
+
+
+def _field(prec):
+    """the worker's field: 0 exact, >0 real mp, <0 complex mp of -prec bits"""
+    if prec == 0:
+        return O.ExactField()
+    return O.ComplexMPField(-prec) if prec < 0 else O.MPField(prec)
+
+
+def _prec_code(F):
+    if not hasattr(F, "ctx"):
+        return 0
+    return -F.ctx.prec if getattr(F, "is_complex", False) else F.ctx.prec
 
 
 def _rows_worker(args):
     sys_, x_np, prec, rows, dc = args
-    F = O.MPField(prec) if prec else O.ExactField()
+    F = _field(prec)
     xs = O.read_x(x_np, F)
     co = O.read_coeffs(sys_, F)
     rhs = O.read_rhs(sys_, F)
@@ -166,7 +183,7 @@ _STAGE = {}
 
 
 def _stage_init(A_part, n, prec):
-    F = O.MPField(prec) if prec else O.ExactField()
+    F = _field(prec)
     _STAGE["A"] = {i: {j: [_unpk(F, v) for v in ser] for j, ser in row.items()} for i, row in A_part.items()}
     _STAGE["n"] = n
     _STAGE["F"] = F
@@ -196,7 +213,7 @@ def parallel_step(sys_, x_np, F, procs=None):
     import multiprocessing as mp
     procs = procs or _procs()
     n, d = sys_.n, sys_.d
-    prec = F.ctx.prec if hasattr(F, "ctx") else 0
+    prec = _prec_code(F)
     ctx = mp.get_context("fork")
     # LPT-ish deal: row costs grow with the monomial sizes
     cost = [sum(int(sys_.mono_ptr[t + 1] - sys_.mono_ptr[t]) for t in O.eq_monomials(sys_, i)) for i in range(n)]
@@ -247,7 +264,7 @@ def parallel_rows(sys_, x_np, F, rows, procs=None):
     """(b_i, A_i) of the listed equations, in worker processes."""
     import multiprocessing as mp
     procs = min(procs or _procs(), len(rows))
-    prec = F.ctx.prec if hasattr(F, "ctx") else 0
+    prec = _prec_code(F)
     chunks = [rows[p::procs] for p in range(procs) if rows[p::procs]]
     with mp.get_context("fork").Pool(len(chunks)) as pool:
         parts = pool.map(_rows_worker, [(sys_, x_np, prec, c, sys_.d) for c in chunks])
@@ -261,3 +278,25 @@ def vacuity(out, s_k, tol):
         m = max(abs(float(v)) for v in dk)
         ratios.append(float("inf") if m == 0 else tol * float(s_k[k]) / m)
     return ratios
+
+
+# ---------------------------------------------------------------------------
+# complex systems (NEXT-2): errors as the modulus of the difference
+# ---------------------------------------------------------------------------
+def cplx_fraction(gpu_c_limbs):
+    """[2][K] limbs -> (re, im) exact Fractions"""
+    return limbs_to_fraction(gpu_c_limbs[0]), limbs_to_fraction(gpu_c_limbs[1])
+
+
+def cerr_ratio(gpu_c_limbs, oracle_val, F, scale: float) -> float:
+    re, im = cplx_fraction(gpu_c_limbs)
+    ore, oim = F.to_fraction(oracle_val)
+    return float(np.hypot(float(re - ore), float(im - oim))) / scale
+
+
+def dense_A0_complex(A, n):
+    M = np.zeros((n, n), complex)
+    for i, row in A.items():
+        for j, ser in row.items():
+            M[i, j] = complex(ser[0])
+    return M

@@ -1,0 +1,146 @@
+"""GPU parity of NEXT-2, complex coefficients (SURVEY
+8(f)): 4M complex md products in the convolutions, complex Householder QR
+(alpha = -(x_0/|x_0|)||x||), unit-circle alpha and c, through the
+C ABI (a complex handle runs the batched kernel), against the complex oracle.
+Tolerance: |gpu - oracle| (modulus) <= tol_p s_k, s_k the running-error scale
+of SURVEY c.4 built from moduli."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import newton as O
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not H.gpu_available():
+        pytest.skip("no CUDA device")
+
+
+def _step_gpu(sys_, x_np, batch=1):
+    import torch
+
+    import paper_2301_12659_b200 as P
+    h = P.NewtonSystem.from_system(sys_, max_batch=batch)
+    x = torch.tensor(x_np, device="cuda:0")
+    res = torch.zeros((sys_.K, 3), dtype=torch.float64, device="cuda:0")
+    h.step(x, res)
+    torch.cuda.synchronize()
+    return x.cpu().numpy(), res.cpu().numpy(), h
+
+
+def _check(sys_, x_np, out, xg, res, nonvacuous=True):
+    n, d, K = sys_.n, sys_.d, sys_.K
+    F = O.field_for(K, complex_=True)
+    sc = O.scales(sys_, x_np)
+    dxf = np.array([[complex(out["dx"][k][i]) for i in range(n)] for k in range(d)])
+    s_k, _ = O.stage_scales(sys_, x_np, H.dense_A0_complex(out["A"], n), dxf, sc["s_b"], sc["s_A"])
+    tol = synth.TOL_P[K]
+    worst, worst_eps = 0.0, 0.0
+    for j in range(n):
+        for k in range(d):
+            r = H.cerr_ratio(xg[:, :, j, k], out["x_new"][j][k], F, float(s_k[k]))
+            worst = max(worst, r / tol)
+            worst_eps = max(worst_eps, r / synth.EPS_P[K])
+    print(f"\ncomplex n={n} d={d} K={K}: max |gpu - oracle| / (tol_p s_k) = {worst:.2e} ({worst_eps:.1f} eps_p)")
+    assert worst <= 1, worst
+    if nonvacuous:
+        vac = H.vacuity(out, s_k, tol)
+        assert max(vac) < 1.0, vac
+    # norms: ||b|| and ||dx|| (moduli summed over i, max over k)
+    nb = float(H.limbs_to_fraction(res[:, 0]))
+    assert abs(nb - float(out["norm_b"])) <= tol * float(sc["s_b"].sum(axis=1).max()) + 1e-300
+    ndx = float(H.limbs_to_fraction(res[:, 2]))
+    assert abs(ndx - float(out["norm_dx"])) <= tol * float(max(s_k)) * n
+
+
+@pytest.mark.parametrize("kind", ["near", "rough", "start"])
+def test_complex_C1_shape(kind):
+    """C1 shape (dim 8, degree 8, double double) with complex data."""
+    sys_ = synth.complex_triangular_system(8, 8, 2, seed=12661)
+    x = synth.make_cx(sys_, kind, seed=3)
+    F = O.field_for(2, complex_=True)
+    out = O.step(sys_, x, F, split=True)
+    xg, res, _ = _step_gpu(sys_, x)
+    _check(sys_, x, out, xg, res, nonvacuous=(kind != "near"))
+
+
+@pytest.mark.parametrize("K", [4, 8])
+def test_complex_medium_all_precisions(K):
+    sys_ = synth.complex_triangular_system(12, 10, K, seed=5)
+    x = synth.make_cx(sys_, "rough", seed=6)
+    out = H.parallel_step(sys_, x, O.field_for(K, complex_=True))
+    xg, res, _ = _step_gpu(sys_, x)
+    _check(sys_, x, out, xg, res)
+
+
+@pytest.mark.slow
+def test_complex_C2_shape():
+    """C2 shape (dim 64, degree 31, quad double) with complex data, 'rough'
+    input: the full complex oracle (parallel_step), non-vacuous."""
+    sys_ = synth.complex_triangular_system(64, 31, 4, seed=12662)
+    x = synth.make_cx(sys_, "rough", seed=1)
+    out = H.parallel_step(sys_, x, O.field_for(4, complex_=True))
+    xg, res, _ = _step_gpu(sys_, x)
+    _check(sys_, x, out, xg, res)
+
+
+def test_complex_closed_form_convergence():
+    """Iterated GPU steps from 'start' converge to exp(alpha t), alpha on the
+    unit circle (quadratic convergence, SURVEY c.3): after ceil(log2(D+2)) + 1
+    steps every coefficient is within tol_p s_k of the closed form."""
+    import math
+
+    import torch
+
+    import paper_2301_12659_b200 as P
+    K, n, D = 4, 6, 15
+    sys_ = synth.complex_triangular_system(n, D, K, seed=9)
+    exact = synth.make_cx(sys_, "exact")
+    F = O.field_for(K, complex_=True)
+    out = O.step(sys_, exact, F, split=True)
+    sc = O.scales(sys_, exact)
+    s_k, _ = O.stage_scales(sys_, exact, H.dense_A0_complex(out["A"], n), np.zeros((D + 1, n)), sc["s_b"],
+                            sc["s_A"])
+    h = P.NewtonSystem.from_system(sys_)
+    x = torch.tensor(synth.make_cx(sys_, "start", seed=10), device="cuda:0")
+    for _ in range(math.ceil(math.log2(D + 2)) + 1):
+        h.step(x)
+    xn = x.cpu().numpy()
+    for j in range(n):
+        for k in range(D + 1):
+            re, im = H.cplx_fraction(xn[:, :, j, k])
+            ere, eim = H.cplx_fraction(exact[:, :, j, k])
+            assert float(np.hypot(float(re - ere), float(im - eim))) <= synth.TOL_P[K] * float(s_k[k]), (j, k)
+
+
+def test_complex_batched_invariance_and_paths():
+    """The batched entry on complex paths: each path of a batch equals the
+    same path run alone (bitwise), and sampled paths meet the oracle."""
+    import torch
+    K, n, D, B = 2, 8, 7, 12
+    base = synth.complex_triangular_system(n, D, K, seed=20)
+    paths = [synth.complex_triangular_system(n, D, K, seed=20 + p) for p in range(B)]
+    xs = np.stack([synth.make_cx(s, "rough", seed=40 + p) for p, s in enumerate(paths)])
+    rhs = np.stack([s.rhs for s in paths])
+    import paper_2301_12659_b200 as P
+    h = P.NewtonSystem.from_system(base, max_batch=B)
+    X = torch.tensor(xs, device="cuda:0")
+    R = torch.tensor(rhs, device="cuda:0")
+    res = torch.zeros((B, K, 3), dtype=torch.float64, device="cuda:0")
+    h.step_batched(X, R, res)
+    Xn = X.cpu().numpy()
+    X1 = torch.tensor(xs[7:8], device="cuda:0")
+    h.step_batched(X1, torch.tensor(rhs[7:8], device="cuda:0"))
+    assert np.array_equal(X1.cpu().numpy()[0], Xn[7])
+    F = O.field_for(K, complex_=True)
+    for p in (0, 7):
+        # the path's own system differs from the handle's only in c and rhs; the
+        # coefficients of the handle are used, so check against the base coefficients
+        sysp = synth.complex_triangular_system(n, D, K, seed=20 + p)
+        sysp.coeff = base.coeff
+        out = O.step(sysp, xs[p], F, split=True)
+        _check(sysp, xs[p], out, Xn[p], res.cpu().numpy()[p])
