@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--no-extras", action="store_true", help="skip the c2/c4/c5 keys")
     p.add_argument("--driver", action="store_true",
                    help="NEXT-1: time whole staggered Newton runs (ns_run_newton) from 'start' to convergence")
+    p.add_argument("--sweep", action="store_true", help="NEXT-3: T6-style eval/diff order sweep (dim 1024, 8d)")
+    p.add_argument("--sweep-dim", type=int, default=1024)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds per oracle sample (1 and N processes)")
     return p.parse_args()
@@ -659,8 +661,73 @@ def run_driver(args):
         print(json.dumps(line))
 
 
+def run_sweep(args):
+    """NEXT-3 order sweep in the style of T6: the paper's shape
+    (one-column system of Eq.(5), dim 1024, octo double) evaluated and
+    differentiated at the orders 1, 2, 3, 5, 8, 12, 18, 27, 41, 62, 64 (the
+    window [0, dc) of ns_set_window truncates every convolution at t^dc,
+    P:495-497); device time of ns_eval_diff per order.  FP64 GFLOPS = the
+    algorithmic md multiply-adds of the truncated convolutions (triangular,
+    S dc(dc+1)/2 + scalings) x FP64 flops per md multiply-add; the paper's
+    own counting (md multiplications x 1742, padded dc^2 products, T2/P:574)
+    beside it as context."""
+    import ctypes
+
+    import torch
+
+    import paper_2301_12659_b200 as P
+    import synth
+    from paper_2301_12659_b200 import perfmodel as PM
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    n = args.sweep_dim
+    K = args.precision or 8
+    sys_ = synth.triangular_system(n, 63, K, seed=12667, name="T6")
+    x = torch.tensor(synth.make_x(sys_, "near", seed=1), device=dev)
+    h = P.NewtonSystem.from_system(sys_, device=local)
+    M = sys_.M
+    ms_ = [int(sys_.mono_ptr[t + 1] - sys_.mono_ptr[t]) for t in range(M)]
+    S = sum(PM.products(m) for m in ms_)
+    L = P.lib()
+    stream = torch.cuda.current_stream()
+    clocks = ClockSampler(smi_index(local))
+    clocks.start()
+    rows = []
+    for dc in (1, 2, 3, 5, 8, 12, 18, 27, 41, 62, 64):
+        h.set_window(0, dc)
+        for _ in range(2):
+            L.ns_eval_diff(h._h, ctypes.c_void_p(x.data_ptr()), None, None, None, ctypes.c_void_p(stream.cuda_stream))
+        reps = 3
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            L.ns_eval_diff(h._h, ctypes.c_void_p(x.data_ptr()), None, None, None, ctypes.c_void_p(stream.cuda_stream))
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        md_fma = S * dc * (dc + 1) // 2 + (M + sum(ms_)) * dc
+        g = PM.flops(md_fma, K) / (ms * 1e-3) * 1e-9
+        paper = S * dc * dc * PM.T2_MUL[K] / (ms * 1e-3) * 1e-9
+        rows.append({"order": dc, "ms": ms, "gflops": g, "paper_convention_gflops": paper})
+    h.set_window(0, sys_.d)
+    clk = clocks.stop()
+    line = {"metric": "eval/diff ms and FP64 GFLOPS per order (T6 sweep)", "value": rows[-1]["gflops"],
+            "unit": "GFLOP/s (FP64, FMA=2)", "n_gpus": 1, "higher_is_better": True, "dtype": "f64",
+            "data": "synthetic (seeded, synth.py; 'near' series)",
+            "config": {"workload": f"T6 shape: dim={n} one-column system (Eq.(5)), {PREC[K]}, eval/diff at orders "
+                                   "1..64 (ns_set_window)", "series_products": S},
+            "orders": rows, "clocks": clk,
+            "paper_T6_context": "V100 1658.4, A100 2568.0, P100 554.7 GFLOPS at order 64, 8d, dim 1024 (paper's "
+                                "convention: md-mul x 1742, padded products)"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    if args.sweep:
+        run_sweep(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     elif args.driver:

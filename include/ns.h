@@ -47,7 +47,7 @@ typedef enum {
   NS_EINVAL = 1,     /* bad argument (NULL pointer, negative size, bad flag)          */
   NS_EPREC = 2,      /* precision not in {2,4,8} or not the handle's precision          */
   NS_EDIM = 3,       /* dim / degree / batch do not match the handle                    */
-  NS_EMONO = 4,      /* malformed monomial list (empty, unsorted, duplicate, >= dim)    */
+  NS_EMONO = 4,      /* malformed monomial list (empty, decreasing, >= dim)            */
   NS_ESINGULAR = 5,  /* (status) an R_jj was exactly zero                  */
   NS_ENONFINITE = 6, /* (status) a norm was not finite                                  */
   NS_ENOMEM = 7,     /* device allocation failed at create                              */
@@ -80,7 +80,8 @@ typedef struct {
   int32_t max_batch;  /* >= 1; paths for ns_newton_series_step_batched            */
   const int32_t* eq_ptr;   /* host [dim+1]: monomials of eq i = [eq_ptr[i], eq_ptr[i+1])  */
   const int32_t* mono_ptr; /* host [M+1]: variables of monomial t = var_idx[mono_ptr[t]..] */
-  const int32_t* var_idx;  /* host: strictly increasing per monomial, < dim (exponent 1)  */
+  const int32_t* var_idx;  /* host: nondecreasing per monomial, < dim; a variable listed e
+                              times has exponent e (NEXT-3 general exponents)   */
   const double* coeff;     /* host [C][K][M] md coefficient c_t; NULL = all ones          */
   const double* rhs;       /* host [C][K][dim][D+1] right-hand side series r_i(t)         */
   int32_t is_complex;      /* 0: real (C = 1); 1: complex coefficients and series (NEXT-2,

@@ -187,14 +187,23 @@ def monomial_value(x, vs, d, F):
 
 
 def monomial_partial(x, vs, j, d, F):
-    """d/dx_j prod_{l in tau} x_l = prod_{l in tau, l != j} x_l  (exponents 0/1,
-    reading R8); the empty product is the series 1 (m = 1, reading R7)."""
-    return product([x[v] for v in vs if v != j], d, F)
+    """d/dx_j prod_{l in tau} x_l.  With exponents 0/1 (reading R8) this is
+    prod_{l in tau, l != j} x_l; the empty product is the series 1 (m = 1,
+    reading R7).  A variable may repeat (x_j^e written as e copies of j: the
+    general exponents of NEXT-3, reading R37): by the product rule
+    the derivative is the sum over the occurrences of j of the product of all
+    the other factors, i.e. e x_j^(e-1) prod_{l != j} x_l^(e_l)."""
+    occ = [q for q, v in enumerate(vs) if v == j]
+    tot = [F.zero] * d
+    for q in occ:
+        p = product([x[v] for r, v in enumerate(vs) if r != q], d, F)
+        tot = [tot[k] + p[k] for k in range(d)]
+    return tot
 
 
 def monomial_partials_split(x, vs, d, F):
-    """The same partials as ``monomial_partial``, each written as the product of
-    the variables before j times the product of the variables after j:
+    """The partials of each occurrence (position q) of the monomial, written as
+    the product of the factors before q times the product of the factors after q:
     prod_{l != j} x_l = (prod_{l < j} x_l) * (prod_{l > j} x_l).  The two
     factor lists are formed once (left to right, right to left).  Pinned
     against ``monomial_partial`` in tests/test_oracle.py; used only to keep
@@ -222,11 +231,12 @@ def evaluate_row(sys, x, coeffs, rhs, i, d, F, split=False):
         c = coeffs[t]
         v = monomial_value(x, vs, d, F)
         val = [val[k] + c * v[k] for k in range(d)]
-        if split:
-            parts = monomial_partials_split(x, vs, d, F)
-        else:
-            parts = [monomial_partial(x, vs, j, d, F) for j in vs]
-        for j, p in zip(vs, parts):
+        if split:  # one partial per occurrence (positional), summed per variable below
+            parts, owners = monomial_partials_split(x, vs, d, F), vs
+        else:      # one partial per distinct variable (all its occurrences)
+            owners = list(dict.fromkeys(vs))
+            parts = [monomial_partial(x, vs, j, d, F) for j in owners]
+        for j, p in zip(owners, parts):
             acc = row.get(j, [F.zero] * d)
             row[j] = [acc[k] + c * p[k] for k in range(d)]
     b = [rhs[i][k] - val[k] for k in range(d)]

@@ -236,13 +236,16 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
     m_max = std::max(m_max, b - a);
     for (int q = a; q < b; ++q) {
       if (desc->var_idx[q] < 0 || desc->var_idx[q] >= n) return NS_EMONO;
-      if (q > a && desc->var_idx[q] <= desc->var_idx[q - 1]) return NS_EMONO;
+      if (q > a && desc->var_idx[q] < desc->var_idx[q - 1]) return NS_EMONO;  // equal: exponent > 1
     }
   }
   if (desc->is_complex != 0 && desc->is_complex != 1) return NS_EINVAL;
   ns_system* s = new (std::nothrow) ns_system();
   if (!s) return NS_ENOMEM;
   s->is_complex = desc->is_complex == 1;
+  for (int t = 0; t < M; ++t)
+    for (int q = desc->mono_ptr[t] + 1; q < desc->mono_ptr[t + 1]; ++q)
+      if (desc->var_idx[q] == desc->var_idx[q - 1]) s->repeats = true;
   s->dev = cuda_device;
   s->n = n;
   s->D = D;

@@ -194,16 +194,21 @@ __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, 
           const V val = (m == 1) ? S::load(xs + (long long)vars[0] * d, lsX, k) : S::load(Fw + (m - 1) * ser, d, k);
           S::store(bb + (long long)k * n, lsV, i, S::fma(S::load(bb + (long long)k * n, lsV, i), S::neg(c), val));
         }
-        for (int t = lane; t < m * d; t += 32) {  // A[i][v_q] += c d x^tau / d x_{v_q}
-          const int q = t % m, k = t / m;
-          V part;
-          if (m == 1) part = (k == 0) ? S::one() : S::zero();
-          else if (m == 2) part = S::load(xs + (long long)vars[1 - q] * d, lsX, k);
-          else if (q == 0) part = S::load(Gw + (m - 2) * ser, d, k);
-          else if (q == m - 1) part = S::load(Fw + (m - 2) * ser, d, k);
-          else part = S::load(Xw + q * ser, d, k);
-          const long long e = dst[q];
-          S::store(A + (long long)k * nnz, lsA, e, S::fma(S::load(A + (long long)k * nnz, lsA, e), c, part));
+        // A[i][v_q] += c d x^tau / d x_{v_q}; repeated variables (exponent > 1)
+        // share an entry: a lane per coefficient then runs over q in order
+        const int qs = s.repeats ? m : 1;
+        for (int t = lane; t < (m / qs) * d; t += 32) {
+          for (int qq = 0; qq < qs; ++qq) {
+            const int q = s.repeats ? qq : t % m, k = s.repeats ? t : t / m;
+            V part;
+            if (m == 1) part = (k == 0) ? S::one() : S::zero();
+            else if (m == 2) part = S::load(xs + (long long)vars[1 - q] * d, lsX, k);
+            else if (q == 0) part = S::load(Gw + (m - 2) * ser, d, k);
+            else if (q == m - 1) part = S::load(Fw + (m - 2) * ser, d, k);
+            else part = S::load(Xw + q * ser, d, k);
+            const long long e = dst[q];
+            S::store(A + (long long)k * nnz, lsA, e, S::fma(S::load(A + (long long)k * nnz, lsA, e), c, part));
+          }
         }
         __syncwarp();
       }

@@ -30,6 +30,8 @@ struct DevSys {
   const double* coeff;  // [K][M]
   const double* rhs;    // [K][n][d]
   int dc;         // active coefficients 0..dc-1 of this step (dc <= d; the staggered window)
+  int repeats;    // some monomial repeats a variable (exponent > 1, NEXT-3): partials of one
+                  // variable accumulate serially (several occurrences share a Jacobian entry)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {

@@ -357,17 +357,22 @@ __global__ void __launch_bounds__(256) evaldiff_jobs_kernel(DevSys s, EdJobs J, 
         md::mdv<K> acc = md::load<K>(bacc, d, k);
         md::store<K>(bacc, d, k, md::fma_acc<K>(acc, md::neg<K>(c), val));
       }
-      for (int t = threadIdx.x; t < m * s.dc; t += blockDim.x) {
-        const int q = t % m, k = t / m;
-        md::mdv<K> part;
-        if (m == 1) part = md::from_double<K>(k == 0 ? 1.0 : 0.0);
-        else if (m == 2) part = md::load<K>(x + (long long)vars[1 - q] * d, xs, k);
-        else if (q == 0) part = md::load_cg<K>(G + (m - 3) * ser, d, k);        // g_{m-2}
-        else if (q == m - 1) part = md::load_cg<K>(F + (m - 3) * ser, d, k);    // f_{m-2}
-        else part = md::load_cg<K>(X + (q - 1) * ser, d, k);                    // d/dx_{q+1}
-        const long long e = dst[q];
-        md::mdv<K> acc = md::load<K>(A + (long long)k * nnz, (long long)d * nnz, e);
-        md::store<K>(A + (long long)k * nnz, (long long)d * nnz, e, md::fma_acc<K>(acc, c, part));
+      // with repeated variables (exponent > 1) several occurrences q share an
+      // entry: one thread per coefficient k then runs over q in order
+      const int qs = s.repeats ? m : 1;
+      for (int t = threadIdx.x; t < (m / qs) * s.dc; t += blockDim.x) {
+        for (int qq = 0; qq < qs; ++qq) {
+          const int q = s.repeats ? qq : t % m, k = s.repeats ? t : t / m;
+          md::mdv<K> part;
+          if (m == 1) part = md::from_double<K>(k == 0 ? 1.0 : 0.0);
+          else if (m == 2) part = md::load<K>(x + (long long)vars[1 - q] * d, xs, k);
+          else if (q == 0) part = md::load_cg<K>(G + (m - 3) * ser, d, k);        // g_{m-2}
+          else if (q == m - 1) part = md::load_cg<K>(F + (m - 3) * ser, d, k);    // f_{m-2}
+          else part = md::load_cg<K>(X + (q - 1) * ser, d, k);                    // d/dx_{q+1}
+          const long long e = dst[q];
+          md::mdv<K> acc = md::load<K>(A + (long long)k * nnz, (long long)d * nnz, e);
+          md::store<K>(A + (long long)k * nnz, (long long)d * nnz, e, md::fma_acc<K>(acc, c, part));
+        }
       }
       __syncthreads();
     }
@@ -436,15 +441,20 @@ __device__ void a0_row(const DevSys& s, const double* __restrict__ x, int i, dou
     const md::mdv<K> sufr = warp_excl_scan_mul<K>(rv);
     const md::mdv<K> suf = md::shfl<K>(sufr, 31 - lane);
     md::mdv<K> P = pre;
-    for (int q = q0; q < min(m, q0 + C); ++q) {
-      md::mdv<K> S = suf;
-      for (int r = min(m, q0 + C) - 1; r > q; --r) S = md::mul<K>(md::load<K>(x + (long long)vars[r] * d, xs, 0), S);
-      const md::mdv<K> part = md::mul<K>(P, S);
-      const long long e = i * rs + (long long)vars[q] * cs;
-      md::store<K>(dst, plane, e, md::fma_acc<K>(md::load<K>(dst, plane, e), c, part));
-      P = md::mul<K>(P, md::load<K>(x + (long long)vars[q] * d, xs, 0));
+    // repeated variables (exponent > 1) share an entry across lanes: the lanes
+    // then add their occurrences in lane order (one lane at a time)
+    for (int L = 0; L < (s.repeats ? 32 : 1); ++L) {
+      if (!s.repeats || lane == L)
+        for (int q = q0; q < min(m, q0 + C); ++q) {
+          md::mdv<K> S = suf;
+          for (int r = min(m, q0 + C) - 1; r > q; --r) S = md::mul<K>(md::load<K>(x + (long long)vars[r] * d, xs, 0), S);
+          const md::mdv<K> part = md::mul<K>(P, S);
+          const long long e = i * rs + (long long)vars[q] * cs;
+          md::store<K>(dst, plane, e, md::fma_acc<K>(md::load<K>(dst, plane, e), c, part));
+          P = md::mul<K>(P, md::load<K>(x + (long long)vars[q] * d, xs, 0));
+        }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 

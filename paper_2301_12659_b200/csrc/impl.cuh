@@ -18,7 +18,7 @@ namespace {
 // device view of the system; dc = active coefficients of this step (window)
 inline DevSys devsys(const ns_system* s) {
   return DevSys{s->n, s->d, s->M, s->nnz, s->m_max, s->eq_ptr, s->mono_ptr, s->var_idx, s->mono_dst,
-                s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs, s->dc};
+                s->row_ptr, s->col_idx, s->job_order, s->coeff, s->rhs, s->dc, s->repeats ? 1 : 0};
 }
 
 template <int K>

@@ -95,6 +95,7 @@ struct ns_system {
   ns_comm* comm = nullptr;     // ns_comm_init (comm.cu), nullptr: one GPU
   // batched (layout, grid and workspace fixed at create: no allocation in a step)
   bool is_complex = false;         // NEXT-2: complex coefficients (batched kernel path)
+  bool repeats = false;            // a monomial repeats a variable (exponent > 1, NEXT-3)
   double* bws = nullptr;
   ns::BLayout bl{};
   int b_grid = 0, b_threads = 256;

@@ -120,7 +120,7 @@ def _csr(eqs: list[list[list[int]]]):
     var_idx = []
     for monos in eqs:
         for vs in monos:
-            assert list(vs) == sorted(set(vs)) and len(vs) >= 1
+            assert list(vs) == sorted(vs) and len(vs) >= 1  # repeats = exponents > 1 (NEXT-3)
             var_idx.extend(vs)
             mono_ptr.append(len(var_idx))
         eq_ptr.append(len(mono_ptr) - 1)
@@ -305,7 +305,8 @@ def inv1mt_system(n: int, D: int, K: int, two_column: bool = False,
 
 def custom_system(eqs: list[list[list[int]]], coeffs: list[float], D: int, K: int,
                   alphas: list[float], name: str = "custom") -> System:
-    """Any 0/1 monomial system with an exp(alpha t) exact solution."""
+    """Any monomial system with an exp(alpha t) exact solution; a variable
+    listed e times in a monomial has exponent e (NEXT-3 general exponents)."""
     n = len(eqs)
     eq_ptr, mono_ptr, var_idx = _csr(eqs)
     rhs = _rhs_exp(eqs, coeffs, alphas, n, D + 1, K)

@@ -67,8 +67,8 @@ def test_create_rejects_bad_descriptors(case, code):
 def test_create_rejects_bad_monomials():
     sys_ = synth.triangular_system(4, 3, 2, seed=1)
     bad = np.array(sys_.var_idx)
-    bad[2] = bad[1]                    # duplicate variable inside monomial 1 -> NS_EMONO
-    d, keep = _desc(sys_, var_idx=bad)
+    bad[5] = 0                         # monomial 2 = [0, 1, 0]: decreasing -> NS_EMONO
+    d, keep = _desc(sys_, var_idx=bad)   # (a repeat, [0, 1, 1], is an exponent: accepted, NEXT-3)
     h = ctypes.c_void_p()
     assert P.lib().ns_system_create(ctypes.byref(d), 0, ctypes.byref(h)) == 4
     bad = np.array(sys_.var_idx)

@@ -555,3 +555,25 @@ def test_library_nccl_comm_single_rank():
     torch.cuda.synchronize()
     assert torch.equal(xa, xb)
     assert h.comm_status() == 0
+
+
+@pytest.mark.parametrize("K", [2, 4, 8])
+def test_general_exponents(K):
+    """NEXT-3 general exponents (reading R37): x_j^e written as e
+    copies of j in a monomial, several monomials per equation; the single-
+    system step and the batched kernel against the oracle, 'rough' input."""
+    sys_ = synth.custom_system([[[0, 0, 1]], [[1, 1], [0]], [[0, 2, 2, 2]], [[1, 3, 3], [2]], [[0, 1, 2, 3, 4, 4]]],
+                               [1.0, -0.5, 1.0, 0.75, 1.0, -0.25, 1.0], 9, K, [0.9, -0.95, 0.875, -1.0, 0.9375])
+    x = synth.make_x(sys_, "rough", seed=7)
+    F = O.field_for(K)
+    _full_parity(sys_, x, F, nonvacuous=True)
+    import torch
+    h = _handle(sys_, max_batch=3)
+    X = torch.tensor(np.stack([x] * 3), device="cuda:0")
+    h.step_batched(X)
+    out = O.step(sys_, x, F, split=True)
+    sc = O.scales(sys_, x)
+    n, D = sys_.n, sys_.D
+    dxf = np.array([[float(out["dx"][k][i]) for i in range(n)] for k in range(D + 1)])
+    s_k, _ = O.stage_scales(sys_, x, H.dense_A0_float(out["A"], n), dxf, sc["s_b"], sc["s_A"])
+    assert H.xnew_errors(sys_, x, out, _np(X)[1], F, s_k) <= 1

@@ -667,3 +667,45 @@ def test_complex_newton_converges_and_fixed_point():
     b, A = O.evaluate(sys_, ex, F)
     dx = O.solve(A, b, n, d, F)
     assert max(abs(v) for dk in dx for v in dk) < F.ctx.mpf(2) ** -400
+
+
+# ---------------------------------------------------------------- NEXT-3: general exponents (repeated variables)
+def test_exponents_closed_forms():
+    """x_j^e as e copies of j (reading R37): at x_j = exp(a_j t) the monomial
+    is exp(S t), S = sum_j e_j a_j, and d/dx_j = e_j exp((S - a_j) t); at
+    x_j = 1/(1-t) a monomial of total degree m has coefficients C(k+m-1, m-1)
+    and d/dx_j = e_j C(k+m-2, m-2).  Both evaluate_row paths agree."""
+    rng = np.random.default_rng(8)
+    alphas = [float(v) for v in rng.uniform(-1, 1, 4)]
+    d = 7
+    x = _exp_x(alphas, d)
+    vs = [0, 0, 0, 2, 3, 3]
+    S = sum(Fraction(alphas[v]) for v in vs)
+    assert O.monomial_value(x, vs, d, FX) == [S ** k / math.factorial(k) for k in range(d)]
+    for j, e in ((0, 3), (2, 1), (3, 2)):
+        Sj = S - Fraction(alphas[j])
+        assert O.monomial_partial(x, vs, j, d, FX) == [e * Sj ** k / math.factorial(k) for k in range(d)]
+    ones = [[Fraction(1)] * d for _ in range(4)]
+    m = len(vs)
+    assert O.monomial_value(ones, vs, d, FX) == [math.comb(k + m - 1, m - 1) for k in range(d)]
+    assert O.monomial_partial(ones, vs, 3, d, FX) == [2 * math.comb(k + m - 2, m - 2) for k in range(d)]
+    sys_ = synth.custom_system([[[0, 0, 1]], [[1, 1], [0]], [[0, 2, 2, 2]]], [1.0, -0.5, 1.0, 0.75], 5, 2,
+                               [0.9, -0.95, 0.875])
+    xs = O.read_x(synth.make_x(sys_, "rough", seed=3), FX)
+    assert O.evaluate(sys_, xs, FX, split=True) == O.evaluate(sys_, xs, FX, split=False)
+
+
+def test_exponents_newton_converges():
+    """Quadratic convergence (SURVEY c.3) on a system with exponents up to 3."""
+    F = O.MPField(600)
+    sys_ = synth.custom_system([[[0, 0]], [[0, 1, 1]], [[1, 2, 2, 2]], [[0, 3], [2, 2]]],
+                               [1.0, 1.0, -0.5, 0.75, 0.25], 6, 8, [0.9, -0.95, 0.875, -1.0])
+    n, d = sys_.n, sys_.d
+    ex = O.read_x(synth.make_x(sys_, "exact"), F)
+    xs = O.read_x(synth.make_x(sys_, "start", seed=5), F)
+    for it in range(1, 5):
+        b, A = O.evaluate(sys_, xs, F)
+        dx = O.solve(A, b, n, d, F)
+        xs = [[xs[j][k] + dx[k][j] for k in range(d)] for j in range(n)]
+        for k in range(min(2 ** it - 1, d)):
+            assert max(abs(xs[j][k] - ex[j][k]) for j in range(n)) < F.num(2.0 ** -380), (it, k)
