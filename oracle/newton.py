@@ -446,10 +446,8 @@ def fabry_ratio(series, F):
 # running-error scales -- float64 magnitudes only
 # --------------------------------------------------------------------------
 def _absconv(a, b, d):
-    c = np.zeros(d)
-    for k in range(d):
-        c[k] = np.dot(a[:k + 1], b[k::-1])
-    return c
+    """truncated convolution of two magnitude series (float64)"""
+    return np.convolve(a, b)[:d]
 
 
 def _mag(planes):
@@ -475,20 +473,25 @@ def scales(sys, x_planes):
     ca = np.hypot(sys.coeff[0, 0], sys.coeff[1, 0]) if cx else np.abs(sys.coeff[0])
     s_b = np.zeros((d, n))
     s_A = {}
+    one = np.zeros(d)
+    one[0] = 1.0
     for i in range(n):
         acc = ra[i].copy()
         for t in eq_monomials(sys, i):
             vs = monomial_vars(sys, t)
-            p = np.zeros(d); p[0] = 1.0
+            m = len(vs)
+            # |.|-products before and after each occurrence q: the partial of
+            # occurrence q is pre[q] * suf[q + 1] (summed per variable, as the
+            # partials themselves; repeated variables = exponents, R37)
+            pre = [one]
             for v in vs:
-                p = _absconv(p, xa[v], d)
-            acc += ca[t] * p
-            for j in vs:
-                q = np.zeros(d); q[0] = 1.0
-                for v in vs:
-                    if v != j:
-                        q = _absconv(q, xa[v], d)
-                s_A[(i, j)] = s_A.get((i, j), np.zeros(d)) + ca[t] * q
+                pre.append(_absconv(pre[-1], xa[v], d))
+            suf = [one] * (m + 1)
+            for q in range(m - 1, -1, -1):
+                suf[q] = _absconv(suf[q + 1], xa[vs[q]], d)
+            acc += ca[t] * pre[m]
+            for q, j in enumerate(vs):
+                s_A[(i, j)] = s_A.get((i, j), np.zeros(d)) + ca[t] * _absconv(pre[q], suf[q + 1], d)
         s_b[:, i] = acc
     return dict(s_b=s_b, s_A=s_A)
 

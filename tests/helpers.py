@@ -30,7 +30,16 @@ def to_frac(F, v) -> Fraction:
 
 
 def err_ratio(gpu_limbs, oracle_val, F, scale: float) -> float:
-    """|gpu - oracle| / scale as a float (scale > 0)."""
+    """|gpu - oracle| / scale as a float (scale > 0).  mp fields: the limbs
+    summed exactly in the field's precision (>= 2x the md bits, so the sum of
+    K nonoverlapping doubles is exact), the difference in the field."""
+    if hasattr(F, "ctx") and not getattr(F, "is_complex", False):
+        c = F.ctx
+        g = c.fsum([c.mpf(float(l)) for l in gpu_limbs])
+        diff = abs(g - oracle_val)
+        if scale <= 0:
+            return 0.0 if diff == 0 else float("inf")
+        return float(diff) / scale
     diff = abs(limbs_to_fraction(gpu_limbs) - to_frac(F, oracle_val))
     if scale <= 0:
         return 0.0 if diff == 0 else float("inf")

@@ -487,18 +487,20 @@ def test_C4_sampled_rows_and_a_posteriori_residual():
     tol = synth.TOL_P[K]
     Aab, dxab, bab = np.abs(g["A"][0]), np.abs(g["dx"][0]), np.abs(g["b"][0])
     worst = 0.0
+    X = O.MPField(1400)  # the products of two 4d numbers and their sums, exact to far below tol_p
+    val = lambda limbs: X.ctx.fsum([X.ctx.mpf(float(l)) for l in limbs])
     for k in range(d):
         rowscale = bab[k].copy()
         for j in range(k + 1):
             rowscale += np.add.reduceat(Aab[j] * dxab[k - j][ci], rp[:-1]) * (np.diff(rp) > 0)
-        scale_k = Fraction(float(rowscale.max()))
-        assert max(bab[k][i] for i in rows) > 1e6 * tol * float(scale_k)  # non-vacuous
+        scale_k = float(rowscale.max())
+        assert max(bab[k][i] for i in rows) > 1e6 * tol * scale_k  # non-vacuous
         for i in rows:
-            r = H.limbs_to_fraction(g["b"][:, k, i])
+            r = val(g["b"][:, k, i])
             for j in range(k + 1):
                 for e in range(rp[i], rp[i + 1]):
-                    r -= H.limbs_to_fraction(g["A"][:, j, e]) * H.limbs_to_fraction(g["dx"][:, k - j, ci[e]])
-            worst = max(worst, float(abs(r) / scale_k) / tol)
+                    r -= val(g["A"][:, j, e]) * val(g["dx"][:, k - j, ci[e]])
+            worst = max(worst, float(abs(r)) / scale_k / tol)
     print(f"\nC4 a-posteriori residual: max |r| / (tol_p scale) = {worst:.2e}")
     assert worst <= 1, worst
     xn = g["x_new"]
