@@ -49,12 +49,13 @@ struct BSer {
   long long ls;     // limb-plane stride
 };
 
-// B truncated convolutions out_b = a_b * b_b (b < B) on one warp: lane per
+// B truncated convolutions out_b = a_b * b_b (b < B; get() returns false for
+// an inactive item) on one warp: lane per
 // output pair (k1, k2 = d-1-k1), both sums in one loop of d+1 terms (k1 + 1
 // terms of c_{k1}, then k2 + 1 of c_{k2}) with the accumulator chosen per
 // term (no divergence), outputs compact series (limb stride ldo).
 template <class S, typename Get>
-__device__ void sconv_warp(int lane, int B, int d, int ldo, Get get) {
+__device__ __forceinline__ void sconv_warp(int lane, int B, int d, int ldo, Get get) {
   using V = typename S::V;
   using Acc = typename S::Acc;
   const int P = (d + 1) / 2;
@@ -66,7 +67,7 @@ __device__ void sconv_warp(int lane, int B, int d, int ldo, Get get) {
       const int tot = (k1 == k2) ? k1 + 1 : d + 1;
       BSer a, b;
       double* out;
-      get(bi, a, b, out);
+      if (get(bi, a, b, out)) {
       Acc a1, a2;
       S::acc_zero(a1);
       S::acc_zero(a2);
@@ -83,12 +84,14 @@ __device__ void sconv_warp(int lane, int B, int d, int ldo, Get get) {
       }
       S::store(out, ldo, k1, S::val(a1));
       if (k2 != k1) S::store(out, ldo, k2, S::val(a2));
+      }
     }
   }
 }
 
-template <class S, int K>
-__global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, double* X, const double* RHS,
+// MB: minimum CTAs per SM the register allocation must allow (launch bounds)
+template <class S, int K, int MB>
+__global__ void __launch_bounds__(256, MB) batched_step_kernel(DevSys s, int batch, double* X, const double* RHS,
                                                            double* RES, double* gws_all, BLayout L,
                                                            long long* trace) {
   using V = typename S::V;
@@ -116,9 +119,7 @@ __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, 
   const long long lsI = (long long)T * TT;
   const long long lsY = (long long)max(n, TT / 2);
   const long long ser = (long long)C * K * d;  // one compact series
-  double* Fw = gws + L.off_ser_g + (size_t)warp * 3 * s.m_max * ser;
-  double* Gw = Fw + s.m_max * ser;
-  double* Xw = Gw + s.m_max * ser;
+  double* Fw = gws + L.off_ser_g + (size_t)warp * 2 * 3 * s.m_max * ser;  // two equations: [2][F, G, X]
   const int ncol = 2 * n;
   int TPC = 1;  // lanes per column of the QR (power of two <= 32, ncol TPC <= NT)
   while (TPC < 32 && ncol * TPC * 2 <= NT) TPC <<= 1;
@@ -145,81 +146,129 @@ __global__ void __launch_bounds__(256) batched_step_kernel(DevSys s, int batch, 
     }
     if (tid == 0) s_next = 0;
     __syncthreads();
-    // ---------------------------------------------------- eval/diff, warp per equation
+    // ---------------------------------------------------- eval/diff, warp per pair of equations
+    // Two equations (consecutive in the LPT order, so of similar cost) advance
+    // in lockstep: their u-th monomials' forward and backward chains share
+    // each layer's convolution batch (up to 4 series x (d+1)/2 output pairs
+    // on the 32 lanes) and their cross products one batch, so the chain layers
+    // do not leave half of the warp idle.  Each equation keeps its own
+    // series (F, G, X per slot) and its own ascending monomial order.
     for (;;) {
       int job = 0;
       if (lane == 0) job = atomicAdd(&s_next, 1);
       job = __shfl_sync(0xffffffffu, job, 0);
-      if (job >= n) break;
-      const int i = s.job_order[job];
-      const int r0 = s.row_ptr[i], len = s.row_ptr[i + 1] - r0;
-      for (int t = lane; t < C * K * d * len; t += 32) A[(long long)(t / len) * nnz + r0 + t % len] = 0.0;
+      if (2 * job >= n) break;
+      const int eqs0 = s.job_order[2 * job];
+      const int eqs1 = (2 * job + 1 < n) ? s.job_order[2 * job + 1] : -1;
+      for (int e2 = 0; e2 < 2; ++e2) {
+        const int i = e2 ? eqs1 : eqs0;
+        if (i < 0) continue;
+        const int r0 = s.row_ptr[i], len = s.row_ptr[i + 1] - r0;
+        for (int t = lane; t < C * K * d * len; t += 32) A[(long long)(t / len) * nnz + r0 + t % len] = 0.0;
+      }
       __syncwarp();
-      for (int tau = s.eq_ptr[i]; tau < s.eq_ptr[i + 1]; ++tau) {
-        const int m0 = s.mono_ptr[tau];
-        const int m = s.mono_ptr[tau + 1] - m0;
-        const int* vars = s.var_idx + m0;
-        const int* dst = s.mono_dst + m0;
-        const V c = S::load(s.coeff, s.M, tau);
+      const int nmono0 = s.eq_ptr[eqs0 + 1] - s.eq_ptr[eqs0];
+      const int nmono1 = (eqs1 >= 0) ? s.eq_ptr[eqs1 + 1] - s.eq_ptr[eqs1] : 0;
+      for (int u = 0; u < max(nmono0, nmono1); ++u) {
+        // the u-th monomial of each equation of the pair (m = 0: none); scalars
+        // selected by e2 (no dynamically indexed local arrays)
+        const int tau0 = (u < nmono0) ? s.eq_ptr[eqs0] + u : -1;
+        const int tau1 = (u < nmono1) ? s.eq_ptr[eqs1] + u : -1;
+        const int m0_ = (tau0 >= 0) ? s.mono_ptr[tau0 + 1] - s.mono_ptr[tau0] : 0;
+        const int m1_ = (tau1 >= 0) ? s.mono_ptr[tau1 + 1] - s.mono_ptr[tau1] : 0;
+        const int* vv0 = s.var_idx + ((tau0 >= 0) ? s.mono_ptr[tau0] : 0);
+        const int* vv1 = s.var_idx + ((tau1 >= 0) ? s.mono_ptr[tau1] : 0);
+        auto TAU = [&](int e2) { return e2 ? tau1 : tau0; };
+        auto MM = [&](int e2) { return e2 ? m1_ : m0_; };
+        auto VV = [&](int e2) { return e2 ? vv1 : vv0; };
         auto xser = [&](int v) { return BSer{xs + (long long)v * d, lsX}; };
-        if (m >= 2) {
-          // layer q: f_q = f_{q-1} * x_{v(q+1)} and g_q = g_{q-1} * x_{v(m-q)} (Eq.(12))
-          for (int q = 1; q <= m - 1; ++q) {
-            const int nb = (q <= m - 2) ? 2 : 1;
-            sconv_warp<S>(lane, nb, d, d, [&](int bi, BSer& pa, BSer& pb, double*& pc) {
-              if (bi == 0) {
-                pa = (q == 1) ? xser(vars[0]) : BSer{Fw + (q - 1) * ser, d};
-                pb = xser(vars[q]);
-                pc = Fw + q * ser;
-              } else {
-                pa = (q == 1) ? xser(vars[m - 1]) : BSer{Gw + (q - 1) * ser, d};
-                pb = xser(vars[m - 1 - q]);
-                pc = Gw + q * ser;
-              }
-            });
-            __syncwarp();
-          }
-          if (m >= 3) {  // cross products d/dx_{v_j} = f_{j-2} * g_{m-j-1}, j = 2..m-1 (Eq.(13))
-            sconv_warp<S>(lane, m - 2, d, d, [&](int bi, BSer& pa, BSer& pb, double*& pc) {
-              const int j = bi + 2;
-              pa = (j - 2 == 0) ? xser(vars[0]) : BSer{Fw + (j - 2) * ser, d};
-              const int gq = m - j - 1;
-              pb = (gq == 0) ? xser(vars[m - 1]) : BSer{Gw + gq * ser, d};
-              pc = Xw + (j - 1) * ser;
-            });
-            __syncwarp();
-          }
+        const int layers = max(m0_, m1_) - 1;
+        // layer q: f_q = f_{q-1} * x_{v(q+1)} and g_q = g_{q-1} * x_{v(m-q)} (Eq.(12))
+        for (int q = 1; q <= layers; ++q) {
+          sconv_warp<S>(lane, 4, d, d, [&](int bi, BSer& pa, BSer& pb, double*& pc) -> bool {
+            const int e2 = bi >> 1, m = MM(e2);
+            const int* vars = VV(e2);
+            double* F = Fw + (size_t)e2 * 3 * s.m_max * ser;
+            double* G = F + s.m_max * ser;
+            if ((bi & 1) == 0) {
+              if (q > m - 1) return false;
+              pa = (q == 1) ? xser(vars[0]) : BSer{F + (q - 1) * ser, d};
+              pb = xser(vars[q]);
+              pc = F + q * ser;
+            } else {
+              if (q > m - 2) return false;
+              pa = (q == 1) ? xser(vars[m - 1]) : BSer{G + (q - 1) * ser, d};
+              pb = xser(vars[m - 1 - q]);
+              pc = G + q * ser;
+            }
+            return true;
+          });
+          __syncwarp();
         }
-        for (int k = lane; k < d; k += 32) {  // b_i -= c x^tau
-          const V val = (m == 1) ? S::load(xs + (long long)vars[0] * d, lsX, k) : S::load(Fw + (m - 1) * ser, d, k);
-          S::store(bb + (long long)k * n, lsV, i, S::fma(S::load(bb + (long long)k * n, lsV, i), S::neg(c), val));
+        // cross products d/dx_{v_j} = f_{j-2} * g_{m-j-1}, j = 2..m-1 (Eq.(13)), both equations
+        const int nx0 = max(0, m0_ - 2), nx1 = max(0, m1_ - 2);
+        if (nx0 + nx1 > 0) {
+          sconv_warp<S>(lane, nx0 + nx1, d, d, [&](int bi, BSer& pa, BSer& pb, double*& pc) -> bool {
+            const int e2 = (bi < nx0) ? 0 : 1, m = MM(e2);
+            const int j = (bi < nx0 ? bi : bi - nx0) + 2;
+            const int* vars = VV(e2);
+            double* F = Fw + (size_t)e2 * 3 * s.m_max * ser;
+            double* G = F + s.m_max * ser;
+            double* X = G + s.m_max * ser;
+            pa = (j - 2 == 0) ? xser(vars[0]) : BSer{F + (j - 2) * ser, d};
+            const int gq = m - j - 1;
+            pb = (gq == 0) ? xser(vars[m - 1]) : BSer{G + gq * ser, d};
+            pc = X + (j - 1) * ser;
+            return true;
+          });
+          __syncwarp();
         }
-        // A[i][v_q] += c d x^tau / d x_{v_q}; repeated variables (exponent > 1)
-        // share an entry: a lane per coefficient then runs over q in order
-        const int qs = s.repeats ? m : 1;
-        for (int t = lane; t < (m / qs) * d; t += 32) {
-          for (int qq = 0; qq < qs; ++qq) {
-            const int q = s.repeats ? qq : t % m, k = s.repeats ? t : t / m;
-            V part;
-            if (m == 1) part = (k == 0) ? S::one() : S::zero();
-            else if (m == 2) part = S::load(xs + (long long)vars[1 - q] * d, lsX, k);
-            else if (q == 0) part = S::load(Gw + (m - 2) * ser, d, k);
-            else if (q == m - 1) part = S::load(Fw + (m - 2) * ser, d, k);
-            else part = S::load(Xw + q * ser, d, k);
-            const long long e = dst[q];
-            S::store(A + (long long)k * nnz, lsA, e, S::fma(S::load(A + (long long)k * nnz, lsA, e), c, part));
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const int m = MM(e2);
+          if (m == 0) continue;
+          const int i = e2 ? eqs1 : eqs0;
+          const int* vars = VV(e2);
+          const int* dst = s.mono_dst + s.mono_ptr[TAU(e2)];
+          const V c = S::load(s.coeff, s.M, TAU(e2));
+          const double* F = Fw + (size_t)e2 * 3 * s.m_max * ser;
+          const double* G = F + s.m_max * ser;
+          const double* X = G + s.m_max * ser;
+          for (int k = lane; k < d; k += 32) {  // b_i -= c x^tau
+            const V val = (m == 1) ? S::load(xs + (long long)vars[0] * d, lsX, k) : S::load(F + (m - 1) * ser, d, k);
+            S::store(bb + (long long)k * n, lsV, i, S::fma(S::load(bb + (long long)k * n, lsV, i), S::neg(c), val));
+          }
+          // A[i][v_q] += c d x^tau / d x_{v_q}; repeated variables (exponent > 1)
+          // share an entry: a lane per coefficient then runs over q in order
+          const int qs = s.repeats ? m : 1;
+          for (int t = lane; t < (m / qs) * d; t += 32) {
+            for (int qq = 0; qq < qs; ++qq) {
+              const int q = s.repeats ? qq : t % m, k = s.repeats ? t : t / m;
+              V part;
+              if (m == 1) part = (k == 0) ? S::one() : S::zero();
+              else if (m == 2) part = S::load(xs + (long long)vars[1 - q] * d, lsX, k);
+              else if (q == 0) part = S::load(G + (m - 2) * ser, d, k);
+              else if (q == m - 1) part = S::load(F + (m - 2) * ser, d, k);
+              else part = S::load(X + q * ser, d, k);
+              const long long e = dst[q];
+              S::store(A + (long long)k * nnz, lsA, e, S::fma(S::load(A + (long long)k * nnz, lsA, e), c, part));
+            }
           }
         }
         __syncwarp();
       }
-      // dense row i of A_0 into W (column major: W[j][i])
-      for (int t = lane; t < C * K * n; t += 32) W[(long long)(t / n) * lsW + (long long)(t % n) * n + i] = 0.0;
-      __syncwarp();
-      for (int t = lane; t < C * K * len; t += 32) {
-        const int ck = t / len, e = r0 + t % len;
-        W[(long long)ck * lsW + (long long)s.col_idx[e] * n + i] = A[(long long)ck * lsA + e];
+      // dense rows of A_0 into W (column major: W[j][i])
+      for (int e2 = 0; e2 < 2; ++e2) {
+        const int i = e2 ? eqs1 : eqs0;
+        if (i < 0) continue;
+        const int r0 = s.row_ptr[i], len = s.row_ptr[i + 1] - r0;
+        for (int t = lane; t < C * K * n; t += 32) W[(long long)(t / n) * lsW + (long long)(t % n) * n + i] = 0.0;
+        __syncwarp();
+        for (int t = lane; t < C * K * len; t += 32) {
+          const int ck = t / len, e = r0 + t % len;
+          W[(long long)ck * lsW + (long long)s.col_idx[e] * n + i] = A[(long long)ck * lsA + e];
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
     __syncthreads();
     if (tr) tr[1] = gtimer();

@@ -86,8 +86,9 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
   } else {
     int ob = s->qr_owner_beta ? 1 : 0;
     void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch, &ob};
-    CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_kernel<K>, dim3(s->grid_qr), dim3(s->qr_threads),
-                                   args, s->qr_smem_reserve, st));
+    const void* qk = s->qr_small_regs ? (const void*)ns::householder_qr_kernel<K, 1>
+                                      : (const void*)ns::householder_qr_kernel<K>;
+    CK(cudaLaunchCooperativeKernel(qk, dim3(s->grid_qr), dim3(s->qr_threads), args, s->qr_smem_reserve, st));
     s->qr_epoch = epoch;
     const long long tot = (long long)K * n * n;
     const int blocks = (int)std::min<long long>((tot + 255) / 256, 4LL * s->sms);
@@ -190,7 +191,12 @@ ns_status setup_grids(ns_system* s) {
   // competed with the owner's chain for the FP64 pipes (C3 QR 7.03 -> 6.92 ms, C4 66.8 -> 63.4)
   s->qr_owner_beta = true;
   if (const char* e = getenv("NS_QR_OWNER_BETA")) s->qr_owner_beta = atoi(e) != 0;
-  s->grid_qr = std::min(s->sms, std::max(1, (2 * s->n + s->qr_threads / 32 - 1) / (s->qr_threads / 32)));
+  // large n (more than the 128-row register window): the register-light
+  // variant at 2 CTAs per SM (NS_QR_SMALLREGS overrides)
+  s->qr_small_regs = s->n > 128;
+  if (const char* e = getenv("NS_QR_SMALLREGS")) s->qr_small_regs = atoi(e) != 0;
+  s->grid_qr = std::min(s->sms * (s->qr_small_regs ? 2 : 1),
+                        std::max(1, (2 * s->n + s->qr_threads / 32 - 1) / (s->qr_threads / 32)));
   // The QR is latency-bound and runs concurrently with eval/diff; a large
   // dynamic shared-memory request keeps eval/diff CTAs off the QR's SMs
   // (NS_QR_RESERVE=0 disables).  Default: reserve when the QR grid is small
@@ -201,8 +207,10 @@ ns_status setup_grids(ns_system* s) {
     bool reserve = 4 * s->grid_qr <= s->sms;
     if (const char* e = getenv("NS_QR_RESERVE")) reserve = atoi(e) != 0;
     s->qr_smem_reserve = reserve ? (size_t)optin : 0;
-    if (reserve)
+    if (reserve) {
       CK(cudaFuncSetAttribute(ns::householder_qr_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+      CK(cudaFuncSetAttribute(ns::householder_qr_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    }
   }
   // cluster QR: the whole [A0 | I] in the shared memory of one cluster of P CTAs
   {
@@ -276,8 +284,12 @@ ns_status setup_grids(ns_system* s) {
     // co-residency bound of the grid QR at its real launch shape (threads and
     // the reserving dynamic shared memory): an override can not exceed it
     int occq = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occq, ns::householder_qr_kernel<K>, s->qr_threads,
-                                                     s->qr_smem_reserve));
+    if (s->qr_small_regs)
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occq, ns::householder_qr_kernel<K, 1>, s->qr_threads,
+                                                       s->qr_smem_reserve));
+    else
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occq, ns::householder_qr_kernel<K>, s->qr_threads,
+                                                       s->qr_smem_reserve));
     if (occq < 1) return NS_ECUDA;
     if (const char* e = getenv("NS_QR_GRID")) s->grid_qr = std::max(1, atoi(e));
     s->grid_qr = std::min(s->grid_qr, s->sms * occq);
@@ -342,7 +354,7 @@ ns::BLayout batched_layout(const ns_system* s, size_t smem_cap_doubles, int thre
   sz[ns::B_KN] = 3 * K * d;
   const int order[ns::B_NARR] = {ns::B_VH, ns::B_BE, ns::B_KN, ns::B_Y, ns::B_X, ns::B_B, ns::B_DX, ns::B_RI, ns::B_W};
   size_t sm = 0;
-  size_t g = (size_t)C * K * d * s->nnz + NW * 3 * (size_t)s->m_max * C * K * d;
+  size_t g = (size_t)C * K * d * s->nnz + NW * 2 * 3 * (size_t)s->m_max * C * K * d;  // A, per-warp series x 2 eqs
   L.off_A_g = 0;
   L.off_ser_g = (size_t)C * K * d * s->nnz;
   L.in_smem = 0;
@@ -362,7 +374,7 @@ ns::BLayout batched_layout(const ns_system* s, size_t smem_cap_doubles, int thre
   return L;
 }
 
-template <class S, int K>
+template <class S, int K, int MB>
 ns_status batched_setup_t(ns_system* s) {
   const int threads = 256;
   int optin = 0;
@@ -377,11 +389,11 @@ ns_status batched_setup_t(ns_system* s) {
   const size_t cap = std::min<size_t>((size_t)optin, (size_t)per_sm / target - 2048) / sizeof(double);
   ns::BLayout L = batched_layout<S, K>(s, cap, threads);
   const size_t smem_bytes = L.smem_doubles * sizeof(double);
-  if (cudaFuncSetAttribute(ns::batched_step_kernel<S, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncSetAttribute(ns::batched_step_kernel<S, K, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem_bytes) != cudaSuccess)
     return NS_ECUDA;
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::batched_step_kernel<S, K>, threads, smem_bytes));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::batched_step_kernel<S, K, MB>, threads, smem_bytes));
   if (occ < 1) return NS_ECUDA;
   s->bl = L;
   s->b_threads = threads;
@@ -399,11 +411,14 @@ ns_status batched_impl(ns_system* s, int batch, double* x, const double* rhs, do
   const int grid = std::min(batch, s->b_grid);
   long long* tr = s->btrace_on ? s->strace_b : nullptr;
   if (s->is_complex)
-    ns::batched_step_kernel<ns::CplxS<K>, K><<<grid, s->b_threads, s->batched_smem, st>>>(ds, batch, x, rhs, res,
-                                                                                           s->bws, s->bl, tr);
+    ns::batched_step_kernel<ns::CplxS<K>, K, 1><<<grid, s->b_threads, s->batched_smem, st>>>(ds, batch, x, rhs, res,
+                                                                                              s->bws, s->bl, tr);
+  else if (s->b_minb == 2)
+    ns::batched_step_kernel<ns::RealS<K>, K, 2><<<grid, s->b_threads, s->batched_smem, st>>>(ds, batch, x, rhs, res,
+                                                                                              s->bws, s->bl, tr);
   else
-    ns::batched_step_kernel<ns::RealS<K>, K><<<grid, s->b_threads, s->batched_smem, st>>>(ds, batch, x, rhs, res,
-                                                                                           s->bws, s->bl, tr);
+    ns::batched_step_kernel<ns::RealS<K>, K, 1><<<grid, s->b_threads, s->batched_smem, st>>>(ds, batch, x, rhs, res,
+                                                                                              s->bws, s->bl, tr);
   s->btrace_grid = grid;
   s->last_launches = 1;
   s->last_stream = st;
@@ -505,7 +520,11 @@ ns_status Impl<K>::batched(ns_system* s, int batch, double* x, const double* rhs
 }
 template <int K>
 ns_status Impl<K>::batched_setup(ns_system* s) {
-  return s->is_complex ? batched_setup_t<ns::CplxS<K>, K>(s) : batched_setup_t<ns::RealS<K>, K>(s);
+  // real: register cap for 2 CTAs per SM (K = 2) unless NS_BATCH_MINB=1
+  s->b_minb = (K == 2) ? 2 : 1;
+  if (const char* e = getenv("NS_BATCH_MINB")) s->b_minb = atoi(e) == 2 ? 2 : 1;
+  if (s->is_complex) return batched_setup_t<ns::CplxS<K>, K, 1>(s);
+  return s->b_minb == 2 ? batched_setup_t<ns::RealS<K>, K, 2>(s) : batched_setup_t<ns::RealS<K>, K, 1>(s);
 }
 template <int K>
 ns_status Impl<K>::md_op(int op, int n, const double* a, const double* b, double* c, cudaStream_t st) {

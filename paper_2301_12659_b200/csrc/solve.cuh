@@ -157,8 +157,11 @@ __device__ __forceinline__ void flag_set(int* f, int v) {
 // column first, keeps it in registers and builds reflector j+1 at once
 // (look-ahead of one column), so the critical path is one column update plus
 // one reflector per step.  n <= 128 rows per lane-register window (4 x 32).
-template <int K>
-__global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const double* __restrict__ x, int n,
+// SR = rows per lane kept in registers (32 SR rows; the rest streamed from L2):
+// SR = 1 (large n, C4) fits 2 CTAs of 256 threads per SM (16 warps: the column
+// updates are throughput work and one warp per SMSP left the FP64 pipe idle)
+template <int K, int SR = (K == 8) ? 2 : 4>
+__global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(DevSys sy, const double* __restrict__ x, int n,
                                                              const double* __restrict__ A0,
                                                              double* W, double* vhead, double* beta,
                                                              double* rdiag, unsigned* bar,
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(256) householder_qr_kernel(DevSys sy, const do
   // after B[j] it adds v0 W[j][c] and applies the update.
   int* fA = flags;
   int* fB = flags + n;
-  constexpr int S = (K == 8) ? 2 : 4;  // rows per lane kept in registers (32 S rows)
+  constexpr int S = SR;  // rows per lane kept in registers (32 S rows)
   for (int j = 0; j < n; ++j) {
     // first owned column > j (the look-ahead column j+1 is always its owner's first)
     int c0 = gw;

@@ -64,6 +64,7 @@ struct ns_system {
   int st2_threads = 64, grid_st2 = 0;  // split stage kernel (stage2_kernel): CTA size and grid
   int qr_threads = 128;        // threads per CTA of the QR kernel
   bool qr_owner_beta = false;  // grid QR: the reflector's owner forms beta (NS_QR_OWNER_BETA)
+  bool qr_small_regs = false;  // grid QR: register-light variant, 2 CTAs per SM (n > 128)
   bool cqr_on = false;         // cluster QR (cqr.cuh) instead of householder_qr_kernel
   int cqr_P = 0, cqr_W = 0, cqr_CPC = 0, cqr_RS = 0, cqr_E = 0;
   size_t cqr_smem = 0;
@@ -98,7 +99,7 @@ struct ns_system {
   bool repeats = false;            // a monomial repeats a variable (exponent > 1, NEXT-3)
   double* bws = nullptr;
   ns::BLayout bl{};
-  int b_grid = 0, b_threads = 256;
+  int b_grid = 0, b_threads = 256, b_minb = 1;
   size_t batched_smem = 0;
   bool btrace_on = false;          // NS_BATCH_TRACE=1 at create: phase stamps of the batched kernel
   long long* strace_b = nullptr;   // [grid][8]

@@ -284,7 +284,7 @@ def vacuity(out, s_k, tol):
     """Per k: tol s_k / max_i |dx_k,i| (< 1: a wrong dx_k would be caught)."""
     ratios = []
     for k, dk in enumerate(out["dx"]):
-        m = max(abs(float(v)) for v in dk)
+        m = max(abs(complex(v)) for v in dk)  # the modulus (complex systems too)
         ratios.append(float("inf") if m == 0 else tol * float(s_k[k]) / m)
     return ratios
 
