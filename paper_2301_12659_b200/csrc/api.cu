@@ -326,8 +326,8 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   ok &= dalloc(&s->A, (size_t)K * d * s->nnz) == cudaSuccess;
   ok &= dalloc(&s->A0, (size_t)K * nn) == cudaSuccess;
   ok &= dalloc(&s->A0q, (size_t)K * nn) == cudaSuccess;
-  ok &= dalloc(&s->qr_flags, 2 * (size_t)n) == cudaSuccess;
-  ok &= cudaMemset(s->qr_flags, 0, sizeof(int) * 2 * n) == cudaSuccess;
+  ok &= dalloc(&s->qr_flags, 3 * (size_t)n) == cudaSuccess;  // A, B, U flags (epoch valued)
+  ok &= cudaMemset(s->qr_flags, 0, sizeof(int) * 3 * n) == cudaSuccess;
   ok &= dalloc(&s->W, (size_t)K * 2 * nn) == cudaSuccess;
   ok &= dalloc(&s->vhead, (size_t)K * n) == cudaSuccess;
   ok &= dalloc(&s->beta, (size_t)K * n) == cudaSuccess;

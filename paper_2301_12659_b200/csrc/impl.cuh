@@ -86,9 +86,15 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
   } else {
     int ob = s->qr_owner_beta ? 1 : 0;
     void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch, &ob};
-    const void* qk = s->qr_small_regs ? (const void*)ns::householder_qr_kernel<K, 1>
-                                      : (const void*)ns::householder_qr_kernel<K>;
-    CK(cudaLaunchCooperativeKernel(qk, dim3(s->grid_qr), dim3(s->qr_threads), args, s->qr_smem_reserve, st));
+    if (s->qr_crit) {
+      void* cargs[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch};
+      CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_crit_kernel<K>, dim3(s->grid_qr),
+                                     dim3(s->qr_threads), cargs, s->qr_smem_reserve, st));
+    } else {
+      const void* qk = s->qr_small_regs ? (const void*)ns::householder_qr_kernel<K, 1>
+                                        : (const void*)ns::householder_qr_kernel<K>;
+      CK(cudaLaunchCooperativeKernel(qk, dim3(s->grid_qr), dim3(s->qr_threads), args, s->qr_smem_reserve, st));
+    }
     s->qr_epoch = epoch;
     const long long tot = (long long)K * n * n;
     const int blocks = (int)std::min<long long>((tot + 255) / 256, 4LL * s->sms);
@@ -197,6 +203,11 @@ ns_status setup_grids(ns_system* s) {
   if (const char* e = getenv("NS_QR_SMALLREGS")) s->qr_small_regs = atoi(e) != 0;
   s->grid_qr = std::min(s->sms * (s->qr_small_regs ? 2 : 1),
                         std::max(1, (2 * s->n + s->qr_threads / 32 - 1) / (s->qr_threads / 32)));
+  // octo double, n <= 128: a dedicated CTA for the dependent reflector chain
+  // (householder_qr_crit_kernel) plus the column CTAs (NS_QR_CRIT overrides)
+  s->qr_crit = K == 8 && s->n <= 128 && !s->qr_small_regs;
+  if (const char* e = getenv("NS_QR_CRIT")) s->qr_crit = atoi(e) != 0 && !s->qr_small_regs;
+  if (s->qr_crit) s->grid_qr = std::min(s->sms, 1 + (2 * s->n - 1 + s->qr_threads / 32 - 1) / (s->qr_threads / 32));
   // The QR is latency-bound and runs concurrently with eval/diff; a large
   // dynamic shared-memory request keeps eval/diff CTAs off the QR's SMs
   // (NS_QR_RESERVE=0 disables).  Default: reserve when the QR grid is small
@@ -207,9 +218,12 @@ ns_status setup_grids(ns_system* s) {
     bool reserve = 4 * s->grid_qr <= s->sms;
     if (const char* e = getenv("NS_QR_RESERVE")) reserve = atoi(e) != 0;
     s->qr_smem_reserve = reserve ? (size_t)optin : 0;
-    if (reserve) {
+    if (reserve) {  // static shared memory of the crit kernel: ~1 KiB below the opt-in
       CK(cudaFuncSetAttribute(ns::householder_qr_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
       CK(cudaFuncSetAttribute(ns::householder_qr_kernel<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+      CK(cudaFuncSetAttribute(ns::householder_qr_crit_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              optin - 2048));
+      if (s->qr_crit) s->qr_smem_reserve = (size_t)optin - 2048;
     }
   }
   // cluster QR: the whole [A0 | I] in the shared memory of one cluster of P CTAs
@@ -284,7 +298,10 @@ ns_status setup_grids(ns_system* s) {
     // co-residency bound of the grid QR at its real launch shape (threads and
     // the reserving dynamic shared memory): an override can not exceed it
     int occq = 0;
-    if (s->qr_small_regs)
+    if (s->qr_crit)
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occq, ns::householder_qr_crit_kernel<K>, s->qr_threads,
+                                                       s->qr_smem_reserve));
+    else if (s->qr_small_regs)
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occq, ns::householder_qr_kernel<K, 1>, s->qr_threads,
                                                        s->qr_smem_reserve));
     else

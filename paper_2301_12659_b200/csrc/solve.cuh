@@ -15,6 +15,7 @@
 #pragma once
 #include "common.cuh"
 #include "evaldiff.cuh"
+#include "scalar.cuh"
 
 namespace ns {
 
@@ -326,6 +327,188 @@ __global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(
         reflector_from_sigma<K>(n, j + 1, sig, x0, W, vhead, beta, rdiag, status, owner_beta != 0);
         __syncwarp();
         if (lane == 0) flag_set(fB + j + 1, epoch);
+      }
+    }
+  }
+}
+
+// CTA-wide sum of unnormalised level sums (one per thread): warp butterflies,
+// then warp 0 combines the warps' levels in warp order; every thread gets the
+// renormalised value.  scratch: K * (blockDim / 32) doubles of shared memory.
+template <int K>
+__device__ md::mdv<K> block_sum_levels(double (&sl)[K], double* scratch) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double s[K];
+#pragma unroll
+  for (int l = 0; l < K; ++l) s[l] = sl[l];
+  lv_group<K>(s, 32);
+  if (lane == 0)
+#pragma unroll
+    for (int l = 0; l < K; ++l) scratch[w * K + l] = s[l];
+  __syncthreads();
+  if (w == 0) {
+    double t[K];
+#pragma unroll
+    for (int l = 0; l < K; ++l) t[l] = (lane < nw) ? scratch[lane * K + l] : 0.0;
+    lv_group<K>(t, 32);
+    const md::mdv<K> v = md::renorm<K, K>(t);
+    if (lane == 0)
+#pragma unroll
+      for (int l = 0; l < K; ++l) scratch[nw * K + l] = v.x[l];
+  }
+  __syncthreads();
+  md::mdv<K> r;
+#pragma unroll
+  for (int l = 0; l < K; ++l) r.x[l] = scratch[nw * K + l];
+  __syncthreads();  // scratch reusable
+  return r;
+}
+
+// Householder QR of [A0 | I] with a dedicated critical CTA.  In the grid QR
+// the look-ahead column's owner warp shares its SM's FP64 pipes with seven
+// warps doing throughput updates, so the dependent chain (update column j+1,
+// its norm, sqrt, reciprocal) ran at a fraction of the pipe: 54 us per step at
+// C3.  Here CTA 0 does only that chain, with all its threads on the column:
+//   step j: wait U[j+1] (column j+1 has H_0..H_{j-1}), apply H_j to it (rows
+//   spread over the CTA, CTA-wide dot), publish A[j+1] (rows > j+1 final),
+//   CTA-wide norm, reflector j+1, publish B[j+1].
+// CTAs 1.. own every other column update: column c (c >= 1, dealt round robin
+// over their warps) takes H_0..H_{c-2} from its owner warp, which publishes
+// U[c] after H_{c-2}; H_{c-1} is the critical CTA's.  Same arithmetic per
+// element as householder_qr_kernel (so the same results up to the order of
+// the dot's partial sums).  Flags (epoch valued): A [n], B [n], U [n].
+template <int K>
+__global__ void __launch_bounds__(256, 1) householder_qr_crit_kernel(DevSys sy, const double* __restrict__ x, int n,
+                                                                    const double* __restrict__ A0, double* W,
+                                                                    double* vhead, double* beta, double* rdiag,
+                                                                    unsigned* bar, unsigned* status, int* flags,
+                                                                    int epoch) {
+  __shared__ double scratch[K * 9];
+  __shared__ double sx0[K];
+  const int ncol = 2 * n;
+  const long long ls = (long long)ncol * n;
+  const int gw = gwarp(), nw = nwarps(), lane = lane_id();
+  const long long tot = (long long)K * ncol * n;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(t % n);
+    const long long lc = t / n;
+    const int c = (int)(lc % ncol), l = (int)(lc / ncol);
+    if (c < n && x) continue;
+    double v;
+    if (c < n) v = A0[((long long)l * n + r) * n + c];
+    else v = (l == 0 && r == c - n) ? 1.0 : 0.0;
+    __stcg(W + (long long)l * ls + (long long)c * n + r, v);
+  }
+  if (x)
+    for (int i = gw; i < n; i += nw) a0_row<K>(sy, x, i, W, ls, 1, n);
+  {
+    GridBarrier gb(bar, (unsigned)(epoch - 1) * (gridDim.x * gridDim.y * gridDim.z));
+    gb.sync();
+  }
+  int* fA = flags;
+  int* fB = flags + n;
+  int* fU = flags + 2 * n;
+  if (blockIdx.x == 0) {
+    // ---------------- the critical chain
+    const int NT = blockDim.x;
+    {  // reflector 0
+      double sl[K];
+      lv_zero<K>(sl);
+      for (int r = threadIdx.x; r < n; r += NT) {
+        const md::mdv<K> v = md::load_cg<K>(W, ls, r);
+        lv_prod<K>(sl, v, v);
+      }
+      const md::mdv<K> sig = block_sum_levels<K>(sl, scratch);
+      if (threadIdx.x < 32) {
+        reflector_from_sigma<K>(n, 0, sig, md::load_cg<K>(W, ls, 0), W, vhead, beta, rdiag, status, true);
+        __syncwarp();
+        if (lane == 0) flag_set(fB, epoch);
+      }
+      __syncthreads();
+    }
+    for (int j = 0; j + 1 < n; ++j) {
+      const int c = j + 1;
+      if (j >= 1) {
+        if (threadIdx.x == 0) flag_wait(fU + c, epoch);
+        __syncthreads();
+      }
+      const md::mdv<K> v0 = md::load_cg<K>(vhead, n, j);
+      const md::mdv<K> bt = md::load_cg<K>(beta, n, j);  // beta itself (the owner forms it)
+      double sl[K];
+      lv_zero<K>(sl);
+      for (int r = j + threadIdx.x; r < n; r += NT) {
+        const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
+        lv_prod<K>(sl, v, md::load_cg<K>(W, ls, (long long)c * n + r));
+      }
+      const md::mdv<K> dot = block_sum_levels<K>(sl, scratch);
+      const md::mdv<K> nw_ = md::neg<K>(md::mul<K>(bt, dot));
+      double sg[K];
+      lv_zero<K>(sg);
+      for (int r = j + threadIdx.x; r < n; r += NT) {
+        const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
+        const md::mdv<K> w = md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)c * n + r), nw_, v);
+        md::store_cg<K>(W, ls, (long long)c * n + r, w);
+        if (r > c) lv_prod<K>(sg, w, w);
+        if (r == c) md::store<K>(sx0, 1, 0, w);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) flag_set(fA + c, epoch);  // rows > c final (cumulative after the barrier)
+      const md::mdv<K> sig = block_sum_levels<K>(sg, scratch);
+      if (threadIdx.x < 32) {
+        reflector_from_sigma<K>(n, c, sig, md::load<K>(sx0, 1, 0), W, vhead, beta, rdiag, status, true);
+        __syncwarp();
+        if (lane == 0) flag_set(fB + c, epoch);
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  // ---------------- the column updates: warps of CTAs 1.., column c (c >= 1)
+  const int rw = (blockIdx.x - 1) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nrw = (gridDim.x - 1) * (blockDim.x >> 5);
+  for (int j = 0; j + 1 < ncol && j < n; ++j) {
+    // owned columns c > j + 1 (c = j + 1 is the critical CTA's at step j)
+    int c0 = 1 + rw;
+    if (c0 <= j + 1) c0 += ((j + 1 - c0) / nrw + 1) * nrw;
+    if (c0 >= ncol) break;
+    if (j > 0) flag_wait(fA + j, epoch);
+    __syncwarp();
+    constexpr int MAXC = 4;
+    md::mdv<K> part[MAXC];
+    int nc = 0;
+    for (int cc = c0; cc < ncol && nc < MAXC; cc += nrw, ++nc) {  // partial dots over rows > j
+      double sl[K];
+      lv_zero<K>(sl);
+      for (int r = j + 1 + lane; r < n; r += 32)
+        lv_prod<K>(sl, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)cc * n + r));
+      part[nc] = md::group_sum_levels<K>(sl, 32);
+    }
+    flag_wait(fB + j, epoch);
+    __syncwarp();
+    const md::mdv<K> v0 = md::load_cg<K>(vhead, n, j);
+    const md::mdv<K> bt = md::load_cg<K>(beta, n, j);
+    int ic = 0;
+    for (int cc = c0; cc < ncol; cc += nrw, ++ic) {
+      md::mdv<K> dot;
+      if (ic < MAXC) {
+        dot = part[ic];
+      } else {
+        double sl[K];
+        lv_zero<K>(sl);
+        for (int r = j + 1 + lane; r < n; r += 32)
+          lv_prod<K>(sl, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)cc * n + r));
+        dot = md::group_sum_levels<K>(sl, 32);
+      }
+      dot = md::fma_acc<K>(dot, v0, md::load_cg<K>(W, ls, (long long)cc * n + j));
+      const md::mdv<K> nw_ = md::neg<K>(md::mul<K>(bt, dot));
+      for (int r = j + lane; r < n; r += 32) {
+        const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
+        md::store_cg<K>(W, ls, (long long)cc * n + r, md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)cc * n + r), nw_, v));
+      }
+      if (cc == j + 2 && cc < n) {  // H_0..H_{cc-2} applied: the critical CTA may take it
+        __syncwarp();
+        if (lane == 0) flag_set(fU + cc, epoch);
       }
     }
   }

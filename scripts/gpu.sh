@@ -26,8 +26,13 @@ case $mode in
     timeout 1200 ncu --metrics $M --clock-control none --csv --log-file gpurun_out/fp64_$1.csv \
       python scripts/one_step.py $1 1 > gpurun_out/fp64_$1.log 2>&1 ;;
   full)
-    timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$2 -c 1 -o gpurun_out/full_$1_$2 \
-      python scripts/one_step.py $1 1 > gpurun_out/full_$1_$2.log 2>&1 ;;
+    # the .ncu-rep stays on the box (gpurun_out is capped at 64 MiB): summaries come back
+    mkdir -p /tmp/ncu
+    timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$2 -c 1 -o /tmp/ncu/full_$1_$2 \
+      python scripts/one_step.py $1 1 > gpurun_out/full_$1_$2.log 2>&1
+    python scripts/ncu_summary.py gpurun_out/full_$1_$2.json /tmp/ncu/full_$1_$2.ncu-rep >> gpurun_out/full_$1_$2.log 2>&1
+    ncu -i /tmp/ncu/full_$1_$2.ncu-rep --page source --csv 2>/dev/null | python scripts/source_hot.py > gpurun_out/full_$1_$2_hot.txt 2>&1
+    ncu -i /tmp/ncu/full_$1_$2.ncu-rep --page source --print-source cuda --csv 2>/dev/null | python scripts/source_hot.py 60 > gpurun_out/full_$1_$2_hot_cuda.txt 2>&1 ;;
   sanitize)
     for C in C1 C2; do
       timeout 1200 compute-sanitizer --tool $1 --print-limit 20 python scripts/one_step.py $C 1 > gpurun_out/sanitize_$1_$C.log 2>&1
