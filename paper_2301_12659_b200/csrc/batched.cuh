@@ -54,8 +54,9 @@ struct BSer {
 // output pair (k1, k2 = d-1-k1), both sums in one loop of d+1 terms (k1 + 1
 // terms of c_{k1}, then k2 + 1 of c_{k2}) with the accumulator chosen per
 // term (no divergence), outputs compact series (limb stride ldo).
-template <class S, typename Get>
-__device__ __forceinline__ void sconv_warp(int lane, int B, int d, int ldo, Get get) {
+// the same with the outputs handed to emit(bi, out, k, value) (an epilogue)
+template <class S, typename Get, typename Emit>
+__device__ __forceinline__ void sconv_warp_emit(int lane, int B, int d, Get get, Emit emit) {
   using V = typename S::V;
   using Acc = typename S::Acc;
   const int P = (d + 1) / 2;
@@ -82,12 +83,18 @@ __device__ __forceinline__ void sconv_warp(int lane, int B, int d, int ldo, Get 
         acc_select(a1, cur, a1, first);
         acc_select(a2, a2, cur, first);
       }
-      S::store(out, ldo, k1, S::val(a1));
-      if (k2 != k1) S::store(out, ldo, k2, S::val(a2));
+      emit(bi, out, k1, S::val(a1));
+      if (k2 != k1) emit(bi, out, k2, S::val(a2));
       }
     }
   }
 }
+
+template <class S, typename Get>
+__device__ __forceinline__ void sconv_warp(int lane, int B, int d, int ldo, Get get) {
+  sconv_warp_emit<S>(lane, B, d, get, [&](int, double* out, int k, const typename S::V& v) { S::store(out, ldo, k, v); });
+}
+
 
 // MB: minimum CTAs per SM the register allocation must allow (launch bounds)
 template <class S, int K, int MB>
@@ -207,8 +214,24 @@ __global__ void __launch_bounds__(256, MB) batched_step_kernel(DevSys s, int bat
         }
         // cross products d/dx_{v_j} = f_{j-2} * g_{m-j-1}, j = 2..m-1 (Eq.(13)), both equations
         const int nx0 = max(0, m0_ - 2), nx1 = max(0, m1_ - 2);
+        // without repeated variables every interior partial (occurrence q = j-1,
+        // 1 <= q <= m-2) has its own A entry: the convolution's epilogue adds
+        // c d/dx_{v_j} x^tau into A directly (no X series round trip); the
+        // boundary partials and m <= 2 follow below, still in monomial order
+        const bool fuse = !s.repeats;
+        auto emit_x = [&](int bi, double* out, int k, const V& v) {
+          if (!fuse) {
+            S::store(out, d, k, v);
+            return;
+          }
+          const int e2 = (bi < nx0) ? 0 : 1;
+          const int q = (bi < nx0 ? bi : bi - nx0) + 1;
+          const long long e = s.mono_dst[s.mono_ptr[TAU(e2)] + q];
+          const V c = S::load(s.coeff, s.M, TAU(e2));
+          S::store(A + (long long)k * nnz, lsA, e, S::fma(S::load(A + (long long)k * nnz, lsA, e), c, v));
+        };
         if (nx0 + nx1 > 0) {
-          sconv_warp<S>(lane, nx0 + nx1, d, d, [&](int bi, BSer& pa, BSer& pb, double*& pc) -> bool {
+          sconv_warp_emit<S>(lane, nx0 + nx1, d, [&](int bi, BSer& pa, BSer& pb, double*& pc) -> bool {
             const int e2 = (bi < nx0) ? 0 : 1, m = MM(e2);
             const int j = (bi < nx0 ? bi : bi - nx0) + 2;
             const int* vars = VV(e2);
@@ -220,7 +243,7 @@ __global__ void __launch_bounds__(256, MB) batched_step_kernel(DevSys s, int bat
             pb = (gq == 0) ? xser(vars[m - 1]) : BSer{G + gq * ser, d};
             pc = X + (j - 1) * ser;
             return true;
-          });
+          }, emit_x);
           __syncwarp();
         }
         for (int e2 = 0; e2 < 2; ++e2) {
@@ -239,10 +262,12 @@ __global__ void __launch_bounds__(256, MB) batched_step_kernel(DevSys s, int bat
           }
           // A[i][v_q] += c d x^tau / d x_{v_q}; repeated variables (exponent > 1)
           // share an entry: a lane per coefficient then runs over q in order
-          const int qs = s.repeats ? m : 1;
-          for (int t = lane; t < (m / qs) * d; t += 32) {
-            for (int qq = 0; qq < qs; ++qq) {
-              const int q = s.repeats ? qq : t % m, k = s.repeats ? t : t / m;
+          // fused: only the boundary occurrences q = 0, m-1 remain (m >= 3)
+          const int mq = (fuse && m >= 3) ? 2 : m;
+          for (int t = lane; t < (mq / (s.repeats ? mq : 1)) * d; t += 32) {
+            for (int qq = 0; qq < (s.repeats ? mq : 1); ++qq) {
+              const int q0 = s.repeats ? qq : t % mq, k = s.repeats ? t : t / mq;
+              const int q = (mq == 2 && m >= 3) ? (q0 == 0 ? 0 : m - 1) : q0;
               V part;
               if (m == 1) part = (k == 0) ? S::one() : S::zero();
               else if (m == 2) part = S::load(xs + (long long)vars[1 - q] * d, lsX, k);
