@@ -395,9 +395,37 @@ __global__ void __launch_bounds__(256, MB) batched_step_kernel(DevSys s, int bat
         __syncthreads();
       }
     }
+    // one diagonal tile (n <= 32): M = R^-1 Q^H once, into the A_0 half of W (the
+    // reflectors and R are no longer needed), so each stage is one matvec
+    // dx_k = M b'_k (same algebra as y = Q^H b'_k, R dx_k = y) and two barriers
+    const bool useM = (T == 1);
+    if (useM) {
+      for (int e = tid; e < n * n; e += NT) {
+        const int r = e / n, j = e % n;
+        Acc a;
+        S::acc_zero(a);
+        for (int c = r; c < n; ++c)
+          S::acc_prod(a, S::load(RI, lsI, (long long)r * TB + c), S::load(W, lsW, (long long)(n + j) * n + c));
+        S::store(W, lsW, (long long)j * n + r, S::val(a));
+      }
+      __syncthreads();
+    }
     if (tr) tr[3] = gtimer();
     // ---------------------------------------------------- stage loop
     for (int k = 0; k < d; ++k) {
+      if (useM) {  // dx_k = M b'_k, M[o][c] = W[c][o]
+        for (int o0 = 0; o0 < n; o0 += NT / TPO) {
+          const int o = o0 + tid / TPO, sub = tid % TPO;
+          const bool act = o < n;
+          Acc a;
+          S::acc_zero(a);
+          for (int c = sub; act && c < n; c += TPO)
+            S::acc_prod(a, S::load(W, lsW, (long long)c * n + o), S::load(bb + (long long)k * n, lsV, c));
+          S::acc_group(a, TPO);
+          if (act && sub == 0) S::store(dxv + (long long)k * n, lsV, o, S::val(a));
+        }
+        __syncthreads();
+      } else {
       // y = Q^H b'_k: (Q^H)[r][c] = W[n + c][r]
       for (int o0 = 0; o0 < n; o0 += NT / TPO) {  // uniform trip count: every lane joins the shuffles
         const int o = o0 + tid / TPO, sub = tid % TPO;
@@ -438,6 +466,7 @@ __global__ void __launch_bounds__(256, MB) batched_step_kernel(DevSys s, int bat
           if (act && sub == 0) S::store(dxv + (long long)k * n, lsV, o, S::val(a));
         }
         __syncthreads();
+      }
       }
       // right-looking updates b'_{k'} -= A_{k'-k} dx_k, k' = k+1..D
       const int npairs = (d - 1 - k) * n;
