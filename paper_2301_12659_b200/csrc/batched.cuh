@@ -308,28 +308,30 @@ __global__ void __launch_bounds__(256, MB) batched_step_kernel(DevSys s, int bat
     {
       const int sub = tid % TPC;
       const int slots = (ncol + NT / TPC - 1) / (NT / TPC);  // column slots per lane group (uniform)
-      for (int j = 0; j < n; ++j) {
-        // reflector j by warp 0
-        if (warp == 0) {
-          Acc sg;
-          S::acc_zero(sg);
-          for (int r = j + lane; r < n; r += 32) S::acc_abs2(sg, S::load(W, lsW, (long long)j * n + r));
-          S::acc_group(sg, 32);
-          const R sig = S::rval(sg);
-          const V x0 = S::load(W, lsW, (long long)j * n + j);
-          const R nrm = md::sqrt<K>(sig);
-          const R ax0 = S::absv(x0);
-          const V alpha = S::neg(S::mul_real(S::phase(x0, ax0), nrm));
-          const V v0 = S::sub(x0, alpha);
-          R bt = md::zero<K>();
-          if (!md::is_zero<K>(sig)) bt = md::recip<K>(md::mul<K>(nrm, md::add<K>(nrm, ax0)));
-          if (lane == 0) {
-            S::store(vh, n, j, v0);
-            md::store<K>(be, n, j, bt);
-            S::store(W, lsW, (long long)j * n + j, alpha);
-          }
+      // reflector c (column c, rows >= c) by one whole warp: alpha, v0, beta
+      auto reflector = [&](int c) {
+        Acc sg;
+        S::acc_zero(sg);
+        for (int r = c + lane; r < n; r += 32) S::acc_abs2(sg, S::load(W, lsW, (long long)c * n + r));
+        S::acc_group(sg, 32);
+        const R sig = S::rval(sg);
+        const V x0 = S::load(W, lsW, (long long)c * n + c);
+        const R nrm = md::sqrt<K>(sig);
+        const R ax0 = S::absv(x0);
+        const V alpha = S::neg(S::mul_real(S::phase(x0, ax0), nrm));
+        const V v0 = S::sub(x0, alpha);
+        R bt = md::zero<K>();
+        if (!md::is_zero<K>(sig)) bt = md::recip<K>(md::mul<K>(nrm, md::add<K>(nrm, ax0)));
+        __syncwarp();
+        if (lane == 0) {
+          S::store(vh, n, c, v0);
+          md::store<K>(be, n, c, bt);
+          S::store(W, lsW, (long long)c * n + c, alpha);
         }
-        __syncthreads();
+      };
+      if (warp == 0) reflector(0);
+      __syncthreads();
+      for (int j = 0; j < n; ++j) {
         const V v0 = S::load(vh, n, j);
         const R bt = md::load<K>(be, n, j);
         for (int sl = 0; sl < slots; ++sl) {
@@ -349,6 +351,13 @@ __global__ void __launch_bounds__(256, MB) batched_step_kernel(DevSys s, int bat
             const long long e = (long long)cg * n + r;
             S::store(W, lsW, e, S::fma(S::load(W, lsW, e), nw, v));
           }
+        }
+        // look-ahead: the warp holding column j+1 (updated by its own lane group
+        // just now) forms reflector j+1 before the step's barrier: one barrier per
+        // step instead of two
+        if (j + 1 < n && warp == (((j + 1) % (NT / TPC)) * TPC) / 32) {
+          __syncwarp();
+          reflector(j + 1);
         }
         __syncthreads();
       }

@@ -35,7 +35,9 @@ case $mode in
     ncu -i /tmp/ncu/full_$1_$2.ncu-rep --page source --print-source cuda --csv 2>/dev/null | python scripts/source_hot.py 60 > gpurun_out/full_$1_$2_hot_cuda.txt 2>&1 ;;
   sanitize)
     for C in C1 C2; do
-      timeout 1200 compute-sanitizer --tool $1 --print-limit 20 python scripts/one_step.py $C 1 > gpurun_out/sanitize_$1_$C.log 2>&1
+      timeout 600 compute-sanitizer --tool $1 --print-limit 20 python scripts/one_step.py $C 0 > gpurun_out/sanitize_$1_$C.log 2>&1
       echo "rc=$?" >> gpurun_out/sanitize_$1_$C.log
-    done ;;
+    done
+    timeout 600 compute-sanitizer --tool $1 --print-limit 20 python scripts/one_step.py C5 0 2 8 > gpurun_out/sanitize_$1_C5b8.log 2>&1
+    echo "rc=$?" >> gpurun_out/sanitize_$1_C5b8.log ;;
 esac

@@ -1,6 +1,6 @@
 """Run `steps` Newton steps of a BASELINE config on cuda:0 after one warm-up
 step (for ncu / compute-sanitizer runs: no timing, no oracle).
-usage: python scripts/one_step.py C3 [steps] [precision]"""
+usage: python scripts/one_step.py C3 [steps] [precision] [batch (C5)]"""
 import os
 import sys
 
@@ -16,7 +16,7 @@ K = int(sys.argv[3]) if len(sys.argv) > 3 else None
 if cfg == "C5":
     import numpy as np
     base = synth.triangular_system(32, 15, K or 2, seed=12665, name="C5")
-    B = 4096
+    B = int(sys.argv[4]) if len(sys.argv) > 4 else 4096
     xs = synth.make_x(base, "near", seed=100)
     X0 = torch.tensor(np.stack([xs] * B), device="cuda:0")
     R = torch.tensor(np.stack([base.rhs] * B), device="cuda:0")
