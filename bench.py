@@ -237,7 +237,7 @@ def oracle_sample(sys_, x_np, budget_s: float, procs: int = 1, rotate: int = 0):
         # rows dealt to the processes by decreasing cost (LPT); the wall time of the slowest counts
         order = sorted(rows, key=lambda i: -rows_cost[i])
         chunks = [order[p::procs] for p in range(procs) if order[p::procs]]
-        with mp.get_context("fork").Pool(len(chunks)) as pool:
+        with mp.get_context("forkserver").Pool(len(chunks)) as pool:
             t_ed = max(pool.map(_oracle_rows, [(sys_, x_np, c) for c in chunks]))
     else:
         t_ed = _oracle_rows((sys_, x_np, rows))
@@ -405,7 +405,7 @@ def extra_c5(args, local, dev, flush, peak, K=2, batch=4096):
     from paper_2301_12659_b200.dist import partition
     ws, rank, _ = dist_env()
     lo, hi = partition(batch, ws, rank)
-    with mp.get_context("fork").Pool(min(16, host_cores())) as pool:
+    with mp.get_context("forkserver").Pool(min(16, host_cores())) as pool:
         data = pool.map(_c5_path, [(p, K) for p in range(lo, hi)], chunksize=16)
     base = synth.triangular_system(32, 15, K, seed=12665, name="C5")
     X0 = torch.tensor(np.stack([d[0] for d in data]), device=dev)

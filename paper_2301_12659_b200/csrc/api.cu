@@ -140,7 +140,8 @@ void free_all(ns_system* s) {
                   s->coeff, s->rhs, s->b, s->A, s->A0, s->W, s->vhead, s->beta, s->rdiag, s->R, s->Qt,
                   s->invR, s->bp, s->dx, s->y, s->part, s->Minv, s->Z, s->pend, s->sflags, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
                   s->bar, s->status, s->bws, s->A0q, s->qr_flags, s->jobs, s->ser_off, s->pool, s->prog, s->left,
-                  s->left_init, s->trace, s->strace, s->sample_rows, s->bpart, s->strace_b};
+                  s->left_init, s->trace, s->strace, s->sample_rows, s->bpart, s->strace_b,
+                  s->wy_blk, s->wy_X, s->wy_T1, s->wy_up, s->wy_u};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& row : s->ev)
@@ -262,6 +263,14 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
   }
   s->TB = 32;
   s->T = (n + s->TB - 1) / s->TB;
+  // blocked WY solve for large n (wy.cuh): Q^T is not formed (NS_WY=0/1 overrides)
+  s->wy = n > 256;
+  if (const char* e = getenv("NS_WY")) s->wy = atoi(e) != 0;
+  if (const char* e = getenv("NS_WY_BW")) {  // block width: a power of two in [2, 256]
+    const int bw = atoi(e);
+    if (bw >= 2 && bw <= 256 && (bw & (bw - 1)) == 0) s->wy_BW = bw;
+  }
+  s->wy_P = (n + s->wy_BW - 1) / s->wy_BW;
   const int L = desc->mono_ptr[M];
   s->h_eq_ptr.assign(desc->eq_ptr, desc->eq_ptr + n + 1);
   s->h_mono_ptr.assign(desc->mono_ptr, desc->mono_ptr + M + 1);
@@ -348,6 +357,14 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
     for (int i = 0; i < n; ++i) maxlen = std::max(maxlen, s->h_row_ptr[i + 1] - s->h_row_ptr[i]);
     s->cmax = std::max(1, (std::max(1, (int)d - 1) * maxlen + 63) / 64);  // ns::UCH = 64
     ok &= dalloc(&s->part, (size_t)K * n * s->cmax) == cudaSuccess;
+  }
+  if (s->wy) {
+    const size_t nb = (size_t)K * 2 * s->wy_P * s->wy_BW * s->wy_BW;
+    ok &= dalloc(&s->wy_blk, nb) == cudaSuccess;
+    ok &= dalloc(&s->wy_X, nb) == cudaSuccess;
+    ok &= dalloc(&s->wy_T1, nb) == cudaSuccess;
+    ok &= dalloc(&s->wy_up, (size_t)K * s->wy_BW) == cudaSuccess;
+    ok &= dalloc(&s->wy_u, (size_t)K * s->wy_BW) == cudaSuccess;
   }
   ok &= dalloc(&s->rbuf, (size_t)K * d * n) == cudaSuccess;
   ok &= dalloc(&s->knorm, (size_t)4 * K * d) == cudaSuccess;  // |b_k|, |r_k|, |dx_k|, |x_k|

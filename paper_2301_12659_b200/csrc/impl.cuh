@@ -9,6 +9,7 @@
 #include "md.cuh"
 #include "solve.cuh"
 #include "system.h"
+#include "wy.cuh"
 
 using ns::DevSys;
 #define CK NS_CK
@@ -42,6 +43,31 @@ ns_status launch_a0(ns_system* s, const double* x, cudaStream_t st) {
   ns::a0_kernel<K><<<blocks, 128, 0, st>>>(ds, x, s->A0q);
   s->last_launches += 1;
   CK(cudaGetLastError());
+  return NS_OK;
+}
+
+// WY path (wy.cuh), after the QR of A_0 alone: R and V row-major, the Gram
+// blocks S_p, then T_p = S_p^{-1} and the inverses of R's diagonal blocks in one
+// cooperative launch.
+template <int K>
+ns_status launch_wy_factors(ns_system* s, cudaStream_t st) {
+  const int n = s->n, BW = s->wy_BW, P = s->wy_P;
+  const long long nn = (long long)n * n;
+  const int ub = (int)std::min<long long>((nn + 255) / 256, 4LL * s->sms);
+  ns::wy_unpack_kernel<K><<<ub, 256, 0, st>>>(n, BW, P, s->W, s->vhead, s->R, s->Minv, s->wy_blk);
+  const long long tasks = (long long)P * BW * BW;
+  const int gb = (int)std::min<long long>((tasks + 7) / 8, 8LL * s->sms);
+  ns::wy_gram_kernel<K><<<gb, 256, 0, st>>>(n, BW, P, s->W, s->vhead, s->beta, s->qr_owner_beta ? 1 : 0, s->wy_blk);
+  CK(cudaMemsetAsync(s->bar + 4, 0, 2 * sizeof(unsigned), st));
+  int nblk = 2 * P;
+  const double* S = s->wy_blk;
+  double *X = s->wy_X, *T1 = s->wy_T1;
+  unsigned* bar2 = s->bar + 4;
+  void* args[] = {&nblk, (void*)&BW, (void*)&S, &X, &T1, &bar2};
+  CK(cudaLaunchCooperativeKernel((const void*)ns::invert_upper_kernel<K>, dim3(s->sms), dim3(256), args, 0, st));
+  s->last_launches += 4;
+  CK(cudaGetLastError());
+  s->qr_cached = true;
   return NS_OK;
 }
 
@@ -85,7 +111,8 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
     s->last_launches += 1;
   } else {
     int ob = s->qr_owner_beta ? 1 : 0;
-    void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch, &ob};
+    int ncol = s->wy ? n : 2 * n;
+    void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch, &ob, &ncol};
     if (s->qr_crit) {
       void* cargs[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch};
       CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_crit_kernel<K>, dim3(s->grid_qr),
@@ -96,6 +123,7 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
       CK(cudaLaunchCooperativeKernel(qk, dim3(s->grid_qr), dim3(s->qr_threads), args, s->qr_smem_reserve, st));
     }
     s->qr_epoch = epoch;
+    if (s->wy) return launch_wy_factors<K>(s, st);
     const long long tot = (long long)K * n * n;
     const int blocks = (int)std::min<long long>((tot + 255) / 256, 4LL * s->sms);
     ns::qr_unpack_kernel<K><<<blocks, 256, 0, st>>>(n, s->W, s->R, s->Qt);
@@ -126,6 +154,17 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
 
 template <int K>
 ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
+  if (s->wy) {
+    CK(cudaMemsetAsync(s->bar + 2, 0, 2 * sizeof(unsigned), st));
+    DevSys ds = devsys(s);
+    ns::WyArgs a{s->b, s->A, s->W, s->Minv, s->vhead, s->R, s->wy_X, s->bp, s->dx, s->y, s->part, s->wy_up, s->wy_u,
+                 s->cmax, s->wy_BW, s->wy_P, k_lo};
+    unsigned* bar = s->bar + 2;
+    void* args[] = {&ds, &a, &bar};
+    CK(cudaLaunchCooperativeKernel((const void*)ns::stage_wy_kernel<K>, dim3(s->grid_st), dim3(256), args, 0, st));
+    s->last_launches += 1;
+    return NS_OK;
+  }
   const int wpb2 = s->st2_threads / 32;
   const int Q = (s->n + wpb2 - 1) / wpb2;
   if (s->use_m && s->stage_split && Q <= s->grid_st2 / 2 && s->dc - k_lo >= 3) {
@@ -201,14 +240,15 @@ ns_status setup_grids(ns_system* s) {
   // variant at 2 CTAs per SM (NS_QR_SMALLREGS overrides)
   s->qr_small_regs = s->n > 128;
   if (const char* e = getenv("NS_QR_SMALLREGS")) s->qr_small_regs = atoi(e) != 0;
+  const int qcols = s->wy ? s->n : 2 * s->n;  // columns of the factored matrix
   s->grid_qr = std::min(s->sms * (s->qr_small_regs ? 2 : 1),
-                        std::max(1, (2 * s->n + s->qr_threads / 32 - 1) / (s->qr_threads / 32)));
+                        std::max(1, (qcols + s->qr_threads / 32 - 1) / (s->qr_threads / 32)));
   // octo double, n <= 128: a dedicated CTA for the dependent reflector chain
   // (householder_qr_crit_kernel) plus the column CTAs (NS_QR_CRIT overrides)
   // measured at C3: 7.39 ms against the grid QR's 6.87 (the column updates on the
   // other CTAs, not the chain, bound the step there), so it is opt-in
   s->qr_crit = false;
-  if (const char* e = getenv("NS_QR_CRIT")) s->qr_crit = atoi(e) != 0 && !s->qr_small_regs;
+  if (const char* e = getenv("NS_QR_CRIT")) s->qr_crit = atoi(e) != 0 && !s->qr_small_regs && !s->wy;
   if (s->qr_crit) s->grid_qr = std::min(s->sms, 1 + (2 * s->n - 1 + s->qr_threads / 32 - 1) / (s->qr_threads / 32));
   // The QR is latency-bound and runs concurrently with eval/diff; a large
   // dynamic shared-memory request keeps eval/diff CTAs off the QR's SMs
@@ -235,7 +275,7 @@ ns_status setup_grids(ns_system* s) {
     s->cqr_on = false;
     // octo double: the trailing updates outweigh the chain on 16 SMs (C3 measured
     // slower than the grid-wide QR), so the cluster QR is for K <= 4
-    bool want = s->n <= 128 && K <= 4;
+    bool want = s->n <= 128 && K <= 4 && !s->wy;
     if (const char* e = getenv("NS_CQR")) want = want && atoi(e) != 0;
     int Pforce = 0, RS = 8;
     if (const char* e = getenv("NS_CQR_P")) Pforce = atoi(e);
@@ -331,6 +371,12 @@ ns_status setup_grids(ns_system* s) {
   }
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::stage_kernel<K>, s->st_threads, 0));
   if (occ < 1) return NS_ECUDA;
+  if (s->wy) {  // cooperative grids of one CTA per SM (256 threads)
+    int o1 = 0, o2 = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, ns::stage_wy_kernel<K>, 256, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, ns::invert_upper_kernel<K>, 256, 0));
+    if (o1 < 1 || o2 < 1) return NS_ECUDA;
+  }
   s->grid_st = s->sms;
   {
     const size_t inv_smem = sizeof(double) * (size_t)K * (2 * s->TB * s->TB + s->TB * s->TB / 2);

@@ -117,8 +117,8 @@ __device__ void apply_reflector(int n, int j, int c, double* W, const double* vh
 template <int K>
 __device__ void reflector_from_sigma(int n, int jj, const md::mdv<K>& sig, const md::mdv<K>& x0, double* W,
                                      double* vhead, double* beta, double* rdiag, unsigned* status,
-                                     bool owner_beta = false) {
-  const long long ls = 2LL * n * n;
+                                     bool owner_beta = false, long long ls = -1) {
+  if (ls < 0) ls = 2LL * n * n;  // W = [A0 | I] (ncol = 2n); the WY path passes n^2
   const int lane = lane_id();
   const md::mdv<K> nrm = md::sqrt<K>(sig);
   const md::mdv<K> alpha = md::is_negative<K>(x0) ? nrm : md::neg<K>(nrm);
@@ -167,8 +167,8 @@ __global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(
                                                              double* W, double* vhead, double* beta,
                                                              double* rdiag, unsigned* bar,
                                                              unsigned* status, int* flags, int epoch,
-                                                             int owner_beta) {
-  const int ncol = 2 * n;
+                                                             int owner_beta, int ncol) {
+  // ncol = 2n: [A0 | I] (R and Q^T in one pass); ncol = n: A0 alone (WY path, wy.cuh)
   const long long ls = (long long)ncol * n;
   const int gw = gwarp(), nw = nwarps(), lane = lane_id();
   // W = [A0 | I], column major.  With x given, A_0 is formed here (warp per
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(
       sig = md::fma_acc<K>(sig, v, v);
     }
     sig = md::group_sum<K>(sig, 32);
-    reflector_from_sigma<K>(n, 0, sig, md::load_cg<K>(W, ls, 0), W, vhead, beta, rdiag, status, owner_beta != 0);
+    reflector_from_sigma<K>(n, 0, sig, md::load_cg<K>(W, ls, 0), W, vhead, beta, rdiag, status, owner_beta != 0, ls);
     __syncwarp();
     if (lane == 0) flag_set(flags + n, epoch);  // B[0]
   }
@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(
   int* fA = flags;
   int* fB = flags + n;
   constexpr int S = SR;  // rows per lane kept in registers (32 S rows)
+  constexpr int QB = (K == 8) ? 2 : 4;  // streamed rows per lane loaded together
   for (int j = 0; j < n; ++j) {
     // first owned column > j (the look-ahead column j+1 is always its owner's first)
     int c0 = gw;
@@ -244,8 +245,20 @@ __global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(
         const int r = j + lane + 32 * q;
         if (r > j && r < n) lv_add(sl, vr[q], wr[q]);
       }
-      for (int r = j + lane + 32 * S; r < n; r += 32)
-        lv_add(sl, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)c0 * n + r));
+      for (int rb = j + lane + 32 * S; rb < n; rb += 32 * QB) {
+        md::mdv<K> wq[QB], vq[QB];
+#pragma unroll
+        for (int q = 0; q < QB; ++q) {
+          const int r = rb + 32 * q;
+          if (r < n) {
+            vq[q] = md::load_cg<K>(W, ls, (long long)j * n + r);
+            wq[q] = md::load_cg<K>(W, ls, (long long)c0 * n + r);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < QB; ++q)
+          if (rb + 32 * q < n) lv_add(sl, vq[q], wq[q]);
+      }
       part[0] = md::group_sum_levels<K>(sl, 32);
     }
     int nc = 1;
@@ -306,17 +319,46 @@ __global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(
             if (r == j + 1) x0 = w;
           }
         }
-        for (int r = j + lane + 32 * S; r < n; r += 32) {
-          const md::mdv<K> w =
-              md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)c * n + r), nw_, md::load_cg<K>(W, ls, (long long)j * n + r));
-          md::store_cg<K>(W, ls, (long long)c * n + r, w);
-          if (look) sg_add(w);
+        // streamed rows in batches of QB per lane: the loads of a batch are
+        // issued together (the stores to W keep the compiler from hoisting the
+        // next iteration's loads, so a row-at-a-time loop paid one L2 round
+        // trip per row: ~29 us per step at n = 1024)
+        for (int rb = j + lane + 32 * S; rb < n; rb += 32 * QB) {
+          md::mdv<K> wq[QB], vq[QB];
+#pragma unroll
+          for (int q = 0; q < QB; ++q) {
+            const int r = rb + 32 * q;
+            if (r < n) {
+              wq[q] = md::load_cg<K>(W, ls, (long long)c * n + r);
+              vq[q] = md::load_cg<K>(W, ls, (long long)j * n + r);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < QB; ++q) {
+            const int r = rb + 32 * q;
+            if (r < n) {
+              const md::mdv<K> w = md::fma_acc<K>(wq[q], nw_, vq[q]);
+              md::store_cg<K>(W, ls, (long long)c * n + r, w);
+              if (look) sg_add(w);
+            }
+          }
         }
       } else {
-        for (int r = j + lane; r < n; r += 32) {
-          const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
-          const md::mdv<K> w = md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)c * n + r), nw_, v);
-          md::store_cg<K>(W, ls, (long long)c * n + r, w);
+        for (int rb = j + lane; rb < n; rb += 32 * QB) {
+          md::mdv<K> wq[QB], vq[QB];
+#pragma unroll
+          for (int q = 0; q < QB; ++q) {
+            const int r = rb + 32 * q;
+            if (r < n) {
+              wq[q] = md::load_cg<K>(W, ls, (long long)c * n + r);
+              vq[q] = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < QB; ++q) {
+            const int r = rb + 32 * q;
+            if (r < n) md::store_cg<K>(W, ls, (long long)c * n + r, md::fma_acc<K>(wq[q], nw_, vq[q]));
+          }
         }
       }
       if (look) {
@@ -324,7 +366,7 @@ __global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(
         if (lane == 0) flag_set(fA + j + 1, epoch);  // column j+1 final below its diagonal
         const md::mdv<K> sig = md::group_sum_levels<K>(sg, 32);
         x0 = md::shfl<K>(x0, 1);  // row j+1 lives in lane 1
-        reflector_from_sigma<K>(n, j + 1, sig, x0, W, vhead, beta, rdiag, status, owner_beta != 0);
+        reflector_from_sigma<K>(n, j + 1, sig, x0, W, vhead, beta, rdiag, status, owner_beta != 0, ls);
         __syncwarp();
         if (lane == 0) flag_set(fB + j + 1, epoch);
       }
@@ -682,63 +724,80 @@ struct StageArgs {
 
 constexpr int UCH = 64;  // update terms per chunk (32 lanes x 2)
 
+// ---- updates: b'_k = b_k - sum_{j=1}^{k} A_j dx_{k-j}, all warps of a
+// cooperative grid.  The k*len_i terms of row i are cut into chunks of UCH;
+// (row, chunk) slots are dealt to all warps, each chunk is summed by one warp
+// (fixed lane order + butterfly), then the chunks of a row are summed in chunk
+// order: deterministic and balanced whatever the row lengths.  Stages below
+// k_lo are inactive (dx = 0).  b'_k also goes to ycopy ([K][n]) if given.
+// Ends without a barrier after the row sums (the caller syncs).
+template <int K>
+__device__ void stage_updates(const DevSys& s, const double* __restrict__ b, const double* __restrict__ A,
+                              const double* dx, double* part, int cmax, double* bp, double* ycopy, int k, int k_lo,
+                              GridBarrier& gb) {
+  const int n = s.n, d = s.d, nnz = s.nnz;
+  const int gw = gwarp(), nw = nwarps(), lane = lane_id();
+  const long long lsV = (long long)d * n;
+  const long long lsA = (long long)d * nnz;
+  const int kk = k - k_lo;
+  if (kk > 0) {
+    int maxlen = 0;
+    for (int i = lane; i < n; i += 32) maxlen = max(maxlen, s.row_ptr[i + 1] - s.row_ptr[i]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
+    const int cpr = (kk * maxlen + UCH - 1) / UCH;  // chunk slots per row
+    const long long lsP = (long long)n * cmax;
+    for (long long slot = gw; slot < (long long)n * cpr; slot += nw) {
+      const int i = (int)(slot / cpr), c = (int)(slot % cpr);
+      const int r0 = s.row_ptr[i], len = s.row_ptr[i + 1] - r0;
+      const int tot = kk * len;
+      if (c * UCH >= tot) continue;  // empty slot (short row), warp-uniform
+      md::mdv<K> acc = md::zero<K>();
+      for (int t = c * UCH + lane; t < min(tot, (c + 1) * UCH); t += 32) {
+        const int j = 1 + t / len;
+        const int e = r0 + t % len;
+        md::mdv<K> aij = md::load<K>(A + (long long)j * nnz, lsA, e);
+        md::mdv<K> xv = md::load_cg<K>(dx + (long long)(k - j) * n, lsV, s.col_idx[e]);
+        acc = md::fma_acc<K>(acc, aij, xv);
+      }
+      acc = md::group_sum<K>(acc, 32);
+      if (lane == 0) md::store_cg<K>(part, lsP, (long long)i * cmax + c, acc);
+    }
+    gb.sync();
+    for (int i = gw; i < n; i += nw) {
+      const int len = s.row_ptr[i + 1] - s.row_ptr[i];
+      const int nc = (kk * len + UCH - 1) / UCH;
+      md::mdv<K> acc = md::zero<K>();
+      for (int c = lane; c < nc; c += 32) acc = md::add<K>(acc, md::load_cg<K>(part, lsP, (long long)i * cmax + c));
+      acc = md::group_sum<K>(acc, 32);
+      if (lane == 0) {
+        const md::mdv<K> v = md::sub<K>(md::load<K>(b + (long long)k * n, lsV, i), acc);
+        md::store_cg<K>(bp + (long long)k * n, lsV, i, v);
+        if (ycopy) md::store_cg<K>(ycopy, n, i, v);
+      }
+    }
+  } else {
+    for (int i = gw; i < n; i += nw)
+      if (lane == 0) {
+        const md::mdv<K> v = md::load<K>(b + (long long)k * n, lsV, i);
+        md::store_cg<K>(bp + (long long)k * n, lsV, i, v);
+        if (ycopy) md::store_cg<K>(ycopy, n, i, v);
+      }
+  }
+}
+
 template <int K>
 __global__ void __launch_bounds__(256) stage_kernel(DevSys s, StageArgs a, unsigned* bar) {
   GridBarrier gb(bar, 0u);
-  const int n = s.n, d = s.d, nnz = s.nnz;
+  const int n = s.n, d = s.d;
   const int gw = gwarp(), nw = nwarps(), lane = lane_id();
   const long long lsV = (long long)d * n;     // limb stride of [K][d][n]
-  const long long lsA = (long long)d * nnz;
   const long long lsM = (long long)n * n;
   const int TB = a.TB;
   const int T = (n + TB - 1) / TB;
   const long long lsI = (long long)T * TB * TB;
   for (int k = a.k_lo; k < s.dc; ++k) {
-    // ---- updates: b'_k = b_k - sum_{j=1}^{k} A_j dx_{k-j}.  The k*len_i terms
-    // of row i are cut into chunks of UCH; (row, chunk) slots are dealt to all
-    // warps, each chunk is summed by one warp (fixed lane order + butterfly),
-    // then the chunks of a row are summed in chunk order: deterministic and
-    // balanced whatever the row lengths.
-    const int kk = k - a.k_lo;  // stages below k_lo are inactive (dx = 0)
-    if (kk > 0) {
-      int maxlen = 0;
-      for (int i = lane; i < n; i += 32) maxlen = max(maxlen, s.row_ptr[i + 1] - s.row_ptr[i]);
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, off));
-      const int cpr = (kk * maxlen + UCH - 1) / UCH;  // chunk slots per row
-      const long long lsP = (long long)n * a.cmax;
-      for (long long slot = gw; slot < (long long)n * cpr; slot += nw) {
-        const int i = (int)(slot / cpr), c = (int)(slot % cpr);
-        const int r0 = s.row_ptr[i], len = s.row_ptr[i + 1] - r0;
-        const int tot = kk * len;
-        if (c * UCH >= tot) continue;  // empty slot (short row), warp-uniform
-        md::mdv<K> acc = md::zero<K>();
-        for (int t = c * UCH + lane; t < min(tot, (c + 1) * UCH); t += 32) {
-          const int j = 1 + t / len;
-          const int e = r0 + t % len;
-          md::mdv<K> aij = md::load<K>(a.A + (long long)j * nnz, lsA, e);
-          md::mdv<K> xv = md::load_cg<K>(a.dx + (long long)(k - j) * n, lsV, s.col_idx[e]);
-          acc = md::fma_acc<K>(acc, aij, xv);
-        }
-        acc = md::group_sum<K>(acc, 32);
-        if (lane == 0) md::store_cg<K>(a.part, lsP, (long long)i * a.cmax + c, acc);
-      }
-      gb.sync();
-      for (int i = gw; i < n; i += nw) {
-        const int len = s.row_ptr[i + 1] - s.row_ptr[i];
-        const int nc = (kk * len + UCH - 1) / UCH;
-        md::mdv<K> acc = md::zero<K>();
-        for (int c = lane; c < nc; c += 32) acc = md::add<K>(acc, md::load_cg<K>(a.part, lsP, (long long)i * a.cmax + c));
-        acc = md::group_sum<K>(acc, 32);
-        if (lane == 0) {
-          md::mdv<K> bk = md::load<K>(a.b + (long long)k * n, lsV, i);
-          md::store_cg<K>(a.bp + (long long)k * n, lsV, i, md::sub<K>(bk, acc));
-        }
-      }
-    } else {
-      for (int i = gw; i < n; i += nw)
-        if (lane == 0) md::store_cg<K>(a.bp + (long long)k * n, lsV, i, md::load<K>(a.b + (long long)k * n, lsV, i));
-    }
+    stage_updates<K>(s, a.b, a.A, a.dx, a.part, a.cmax, a.bp, nullptr, k, a.k_lo, gb);
     gb.sync();
     if (a.M) {
       // ---- dx_k = M b'_k  (qhb and bs in one matvec)

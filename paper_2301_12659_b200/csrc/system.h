@@ -42,6 +42,11 @@ struct ns_system {
   double *part = nullptr;
   double *Minv = nullptr, *Z = nullptr;  // M = R^{-1} Q^T and its scratch
   bool use_m = true;                  // false: per-stage tiled back substitution (NS_TILED_BS)
+  // blocked WY solve (wy.cuh; n > 256 by default, NS_WY overrides): QR of A_0 alone,
+  // T_p of BW-reflector blocks, per-stage Q^T b by blocks; V (row-major) lives in Minv
+  bool wy = false;
+  int wy_BW = 256, wy_P = 0;
+  double *wy_blk = nullptr, *wy_X = nullptr, *wy_T1 = nullptr, *wy_up = nullptr, *wy_u = nullptr;
   int cmax = 1;
   double *y = nullptr, *rbuf = nullptr, *knorm = nullptr, *res_tmp = nullptr, *ws = nullptr;
   int* job_counter = nullptr;

@@ -223,7 +223,10 @@ def parallel_step(sys_, x_np, F, procs=None):
     procs = procs or _procs()
     n, d = sys_.n, sys_.d
     prec = _prec_code(F)
-    ctx = mp.get_context("fork")
+    # forkserver, not fork: the pytest process has CUDA (and its threads)
+    # initialised; a forked child can deadlock on a lock held at fork time
+    # (it hung the C3 full-parity test once)
+    ctx = mp.get_context("forkserver")
     # LPT-ish deal: row costs grow with the monomial sizes
     cost = [sum(int(sys_.mono_ptr[t + 1] - sys_.mono_ptr[t]) for t in O.eq_monomials(sys_, i)) for i in range(n)]
     order = sorted(range(n), key=lambda i: -cost[i])
@@ -275,7 +278,7 @@ def parallel_rows(sys_, x_np, F, rows, procs=None):
     procs = min(procs or _procs(), len(rows))
     prec = _prec_code(F)
     chunks = [rows[p::procs] for p in range(procs) if rows[p::procs]]
-    with mp.get_context("fork").Pool(len(chunks)) as pool:
+    with mp.get_context("forkserver").Pool(len(chunks)) as pool:
         parts = pool.map(_rows_worker, [(sys_, x_np, prec, c, sys_.d) for c in chunks])
     return _unpack_rows(F, parts)
 

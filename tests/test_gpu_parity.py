@@ -455,6 +455,30 @@ def test_n160_grid_qr_streaming_and_stage_paths(split):
         _full_parity(sys_, x, F, out=out, nonvacuous=True)
 
 
+@pytest.mark.parametrize("K,bw", [(2, 16), (4, 32), (8, 128), (4, 128)])
+def test_wy_solve_path(K, bw):
+    """Blocked WY solve (wy.cuh; the default for n > 256): QR of A_0 alone,
+    T_p = S_p^-1 per block of bw reflectors, per stage Q^T b'_k by blocks and
+    back substitution by bw-row tiles.  Forced on at n = 40 (NS_WY=1): several
+    blocks and a partial last block (bw = 16, 32), one identity-padded block
+    (bw = 128); full oracle parity on 'rough' input."""
+    # degree 7 at 2d: from k = 8 on tol_p s_k exceeds |dx_k| (a vacuous check)
+    sys_ = synth.triangular_system(40, 7 if K == 2 else 12, K, seed=49)
+    x = synth.make_x(sys_, "rough", seed=50)
+    with _env(NS_WY=1, NS_WY_BW=bw):
+        _full_parity(sys_, x, O.field_for(K), nonvacuous=True)
+
+
+def test_wy_solve_path_n300_banded():
+    """n = 300 > 256 takes the WY path by default: three blocks of 128 (the last
+    partial), the 2-column banded structure of C4 with signed md coefficients."""
+    sys_ = synth.banded_two_column_system(300, 8, 6, 4, seed=51)
+    x = synth.make_x(sys_, "rough", seed=52)
+    F = O.field_for(4)
+    out = H.parallel_step(sys_, x, F)
+    _full_parity(sys_, x, F, out=out, nonvacuous=True)
+
+
 @pytest.mark.parametrize("owner", [0, 1])
 def test_grid_qr_owner_beta_modes(owner):
     """NS_QR_OWNER_BETA: the reflector's owner forms beta (1, default) or each
@@ -505,11 +529,32 @@ def test_C4_sampled_rows_and_a_posteriori_residual():
             worst = max(worst, float(abs(r)) / scale_k / tol)
     print(f"\nC4 a-posteriori residual: max |r| / (tol_p scale) = {worst:.2e}")
     assert worst <= 1, worst
+    # (3) the step's own update dx' = x_new - x (the step forms A_0 inside the QR
+    # kernel, a0_row, so its dx is not bitwise the solve's): the same
+    # a-posteriori residual check on the sampled equations
     xn = g["x_new"]
-    for i in rows:
-        for k in (0, 7, d - 1):
-            want = H.limbs_to_fraction(x[:, i, k]) + H.limbs_to_fraction(g["dx"][:, k, i])
-            assert abs(H.limbs_to_fraction(xn[:, i, k]) - want) <= Fraction(tol) * abs(want)
+    worst2 = 0.0
+    cols = sorted({int(ci[e]) for i in rows for e in range(rp[i], rp[i + 1])})
+    dxs = {(c, k): val(xn[:, c, k]) - val(x[:, c, k]) for c in cols for k in range(d)}
+    # x_new = x (+) dx is one md addition: |x_new - (x + dx)| <= 8 eps_p (|x| + |dx|)
+    # (reading R32, c_4 <= 8), which A_j carries into the residual
+    xdx = np.abs(x[0]).T + dxab  # [d][n]
+    for k in range(d):
+        rowscale = bab[k].copy()
+        addb = np.zeros(sys_.n)
+        for j in range(k + 1):
+            rowscale += np.add.reduceat(Aab[j] * dxab[k - j][ci], rp[:-1]) * (np.diff(rp) > 0)
+            addb += np.add.reduceat(Aab[j] * xdx[k - j][ci], rp[:-1]) * (np.diff(rp) > 0)
+        scale_k = float(rowscale.max())
+        for i in rows:
+            r = val(g["b"][:, k, i])
+            for j in range(k + 1):
+                for e in range(rp[i], rp[i + 1]):
+                    r -= val(g["A"][:, j, e]) * dxs[(int(ci[e]), k - j)]
+            bound = tol * scale_k + 8 * synth.EPS_P[K] * float(addb[i])
+            worst2 = max(worst2, float(abs(r)) / bound)
+    print(f"C4 a-posteriori residual of the step's x_new - x: {worst2:.2e}")
+    assert worst2 <= 1, worst2
 
 
 def test_library_row_replication_kernels_bitwise():
