@@ -112,9 +112,10 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
   } else {
     int ob = s->qr_owner_beta ? 1 : 0;
     int ncol = s->wy ? n : 2 * n;
-    void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch, &ob, &ncol};
+    int il = s->qr_interleave ? 1 : 0;
+    void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch, &ob, &ncol, &il};
     if (s->qr_crit) {
-      void* cargs[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch};
+      void* cargs[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch, &ncol, &il};
       CK(cudaLaunchCooperativeKernel((const void*)ns::householder_qr_crit_kernel<K>, dim3(s->grid_qr),
                                      dim3(s->qr_threads), cargs, s->qr_smem_reserve, st));
     } else {
@@ -239,17 +240,24 @@ ns_status setup_grids(ns_system* s) {
   // large n (more than the 128-row register window): the register-light
   // variant at 2 CTAs per SM (NS_QR_SMALLREGS overrides)
   s->qr_small_regs = s->n > 128;
+  // columns spread over the CTAs on the WY path (n > 256, every SM busy to the end);
+  // [A0 | I] (n <= 256) keeps contiguous ownership (C3 measured 6.94 vs 7.23 ms)
+  s->qr_interleave = s->wy;
+  if (const char* e = getenv("NS_QR_INTERLEAVE")) s->qr_interleave = atoi(e) != 0;
   if (const char* e = getenv("NS_QR_SMALLREGS")) s->qr_small_regs = atoi(e) != 0;
   const int qcols = s->wy ? s->n : 2 * s->n;  // columns of the factored matrix
   s->grid_qr = std::min(s->sms * (s->qr_small_regs ? 2 : 1),
                         std::max(1, (qcols + s->qr_threads / 32 - 1) / (s->qr_threads / 32)));
-  // octo double, n <= 128: a dedicated CTA for the dependent reflector chain
-  // (householder_qr_crit_kernel) plus the column CTAs (NS_QR_CRIT overrides)
-  // measured at C3: 7.39 ms against the grid QR's 6.87 (the column updates on the
-  // other CTAs, not the chain, bound the step there), so it is opt-in
-  s->qr_crit = false;
-  if (const char* e = getenv("NS_QR_CRIT")) s->qr_crit = atoi(e) != 0 && !s->qr_small_regs && !s->wy;
-  if (s->qr_crit) s->grid_qr = std::min(s->sms, 1 + (2 * s->n - 1 + s->qr_threads / 32 - 1) / (s->qr_threads / 32));
+  // a dedicated CTA for the dependent reflector chain (householder_qr_crit_kernel)
+  // plus the column CTAs (NS_QR_CRIT overrides): at C3 ([A0 | I], 8d) measured 9.05
+  // against the grid QR's 6.86 ms (the owner warps' column updates bound the step
+  // there), so it is off for n <= 256; WY path (n > 256): the critical-chain CTA is the default (C4 QR 32.0 -> 24.0 ms)
+  s->qr_crit = s->wy;
+  if (const char* e = getenv("NS_QR_CRIT")) s->qr_crit = atoi(e) != 0;
+  if (s->qr_crit) {
+    s->qr_small_regs = false;
+    s->grid_qr = std::min(s->sms, 1 + (qcols - 1 + s->qr_threads / 32 - 1) / (s->qr_threads / 32));
+  }
   // The QR is latency-bound and runs concurrently with eval/diff; a large
   // dynamic shared-memory request keeps eval/diff CTAs off the QR's SMs
   // (NS_QR_RESERVE=0 disables).  Default: reserve when the QR grid is small

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(
                                                              double* W, double* vhead, double* beta,
                                                              double* rdiag, unsigned* bar,
                                                              unsigned* status, int* flags, int epoch,
-                                                             int owner_beta, int ncol) {
+                                                             int owner_beta, int ncol, int interleave) {
   // ncol = 2n: [A0 | I] (R and Q^T in one pass); ncol = n: A0 alone (WY path, wy.cuh)
   const long long ls = (long long)ncol * n;
   const int gw = gwarp(), nw = nwarps(), lane = lane_id();
@@ -191,7 +191,13 @@ __global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(
     GridBarrier gb(bar, (unsigned)(epoch - 1) * (gridDim.x * gridDim.y * gridDim.z));
     gb.sync();
   }
-  if (gw == 0) {  // reflector 0 (owner of column 0)
+  // column ownership: warp w of CTA b owns columns ow, ow + nw, ... with
+  // ow = w G + b (interleave = 1): every SM holds columns spread over the whole
+  // range, so the SMs stay busy until the end (with ow = global warp id, CTA b
+  // owned columns 8b..8b+7 and the SMs of the early columns idled: half the
+  // GPU for the second half of the factorisation)
+  const int ow = interleave ? (int)((threadIdx.x >> 5) * gridDim.x + blockIdx.x) : gw;
+  if (ow == 0) {  // reflector 0 (owner of column 0)
     md::mdv<K> sig = md::zero<K>();
     for (int r = lane; r < n; r += 32) {
       const md::mdv<K> v = md::load_cg<K>(W, ls, r);
@@ -210,11 +216,10 @@ __global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(
   int* fA = flags;
   int* fB = flags + n;
   constexpr int S = SR;  // rows per lane kept in registers (32 S rows)
-  constexpr int QB = (K == 8) ? 2 : 4;  // streamed rows per lane loaded together
   for (int j = 0; j < n; ++j) {
     // first owned column > j (the look-ahead column j+1 is always its owner's first)
-    int c0 = gw;
-    if (c0 <= j) c0 += ((j - gw) / nw + 1) * nw;
+    int c0 = ow;
+    if (c0 <= j) c0 += ((j - ow) / nw + 1) * nw;
     if (c0 >= ncol) break;  // nothing left for this warp
     if (j > 0) flag_wait(fA + j, epoch);  // column 0 was final at the start
     __syncwarp();
@@ -245,20 +250,8 @@ __global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(
         const int r = j + lane + 32 * q;
         if (r > j && r < n) lv_add(sl, vr[q], wr[q]);
       }
-      for (int rb = j + lane + 32 * S; rb < n; rb += 32 * QB) {
-        md::mdv<K> wq[QB], vq[QB];
-#pragma unroll
-        for (int q = 0; q < QB; ++q) {
-          const int r = rb + 32 * q;
-          if (r < n) {
-            vq[q] = md::load_cg<K>(W, ls, (long long)j * n + r);
-            wq[q] = md::load_cg<K>(W, ls, (long long)c0 * n + r);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < QB; ++q)
-          if (rb + 32 * q < n) lv_add(sl, vq[q], wq[q]);
-      }
+      for (int r = j + lane + 32 * S; r < n; r += 32)
+        lv_add(sl, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)c0 * n + r));
       part[0] = md::group_sum_levels<K>(sl, 32);
     }
     int nc = 1;
@@ -319,46 +312,17 @@ __global__ void __launch_bounds__(256, (SR == 1) ? 2 : 1) householder_qr_kernel(
             if (r == j + 1) x0 = w;
           }
         }
-        // streamed rows in batches of QB per lane: the loads of a batch are
-        // issued together (the stores to W keep the compiler from hoisting the
-        // next iteration's loads, so a row-at-a-time loop paid one L2 round
-        // trip per row: ~29 us per step at n = 1024)
-        for (int rb = j + lane + 32 * S; rb < n; rb += 32 * QB) {
-          md::mdv<K> wq[QB], vq[QB];
-#pragma unroll
-          for (int q = 0; q < QB; ++q) {
-            const int r = rb + 32 * q;
-            if (r < n) {
-              wq[q] = md::load_cg<K>(W, ls, (long long)c * n + r);
-              vq[q] = md::load_cg<K>(W, ls, (long long)j * n + r);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < QB; ++q) {
-            const int r = rb + 32 * q;
-            if (r < n) {
-              const md::mdv<K> w = md::fma_acc<K>(wq[q], nw_, vq[q]);
-              md::store_cg<K>(W, ls, (long long)c * n + r, w);
-              if (look) sg_add(w);
-            }
-          }
+        for (int r = j + lane + 32 * S; r < n; r += 32) {
+          const md::mdv<K> w =
+              md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)c * n + r), nw_, md::load_cg<K>(W, ls, (long long)j * n + r));
+          md::store_cg<K>(W, ls, (long long)c * n + r, w);
+          if (look) sg_add(w);
         }
       } else {
-        for (int rb = j + lane; rb < n; rb += 32 * QB) {
-          md::mdv<K> wq[QB], vq[QB];
-#pragma unroll
-          for (int q = 0; q < QB; ++q) {
-            const int r = rb + 32 * q;
-            if (r < n) {
-              wq[q] = md::load_cg<K>(W, ls, (long long)c * n + r);
-              vq[q] = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < QB; ++q) {
-            const int r = rb + 32 * q;
-            if (r < n) md::store_cg<K>(W, ls, (long long)c * n + r, md::fma_acc<K>(wq[q], nw_, vq[q]));
-          }
+        for (int r = j + lane; r < n; r += 32) {
+          const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
+          const md::mdv<K> w = md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)c * n + r), nw_, v);
+          md::store_cg<K>(W, ls, (long long)c * n + r, w);
         }
       }
       if (look) {
@@ -406,17 +370,19 @@ __device__ md::mdv<K> block_sum_levels(double (&sl)[K], double* scratch) {
   return r;
 }
 
-// Householder QR of [A0 | I] with a dedicated critical CTA.  In the grid QR
+// Householder QR of [A0 | I] (or A0 alone) with a dedicated critical CTA.  In the grid QR
 // the look-ahead column's owner warp shares its SM's FP64 pipes with seven
 // warps doing throughput updates, so the dependent chain (update column j+1,
 // its norm, sqrt, reciprocal) ran at a fraction of the pipe: 54 us per step at
 // C3.  Here CTA 0 does only that chain, with all its threads on the column:
-//   step j: wait U[j+1] (column j+1 has H_0..H_{j-1}), apply H_j to it (rows
-//   spread over the CTA, CTA-wide dot), publish A[j+1] (rows > j+1 final),
-//   CTA-wide norm, reflector j+1, publish B[j+1].
+//   step j: wait U[j+1] (column j+1 has H_0..H_{j-2}), apply H_{j-1} and H_j
+//   to it (rows spread over the CTA, CTA-wide dots), publish A[j+1] (rows > j+1
+//   final), CTA-wide norm, reflector j+1, publish B[j+1].
 // CTAs 1.. own every other column update: column c (c >= 1, dealt round robin
-// over their warps) takes H_0..H_{c-2} from its owner warp, which publishes
-// U[c] after H_{c-2}; H_{c-1} is the critical CTA's.  Same arithmetic per
+// over their warps) takes H_0..H_{c-3} from its owner warp, which publishes
+// U[c] after H_{c-3}; H_{c-2} and H_{c-1} are the critical CTA's (look-ahead of
+// two: with one, the owner warp's update of the next column by H_{c-2} sat on
+// the chain).  Same arithmetic per
 // element as householder_qr_kernel (so the same results up to the order of
 // the dot's partial sums).  Flags (epoch valued): A [n], B [n], U [n].
 template <int K>
@@ -424,10 +390,10 @@ __global__ void __launch_bounds__(256, 1) householder_qr_crit_kernel(DevSys sy, 
                                                                     const double* __restrict__ A0, double* W,
                                                                     double* vhead, double* beta, double* rdiag,
                                                                     unsigned* bar, unsigned* status, int* flags,
-                                                                    int epoch) {
+                                                                    int epoch, int ncol, int interleave) {
   __shared__ double scratch[K * 9];
   __shared__ double sx0[K];
-  const int ncol = 2 * n;
+  // ncol = 2n: [A0 | I]; ncol = n: A0 alone (WY path)
   const long long ls = (long long)ncol * n;
   const int gw = gwarp(), nw = nwarps(), lane = lane_id();
   const long long tot = (long long)K * ncol * n;
@@ -463,7 +429,7 @@ __global__ void __launch_bounds__(256, 1) householder_qr_crit_kernel(DevSys sy, 
       }
       const md::mdv<K> sig = block_sum_levels<K>(sl, scratch);
       if (threadIdx.x < 32) {
-        reflector_from_sigma<K>(n, 0, sig, md::load_cg<K>(W, ls, 0), W, vhead, beta, rdiag, status, true);
+        reflector_from_sigma<K>(n, 0, sig, md::load_cg<K>(W, ls, 0), W, vhead, beta, rdiag, status, true, ls);
         __syncwarp();
         if (lane == 0) flag_set(fB, epoch);
       }
@@ -471,34 +437,40 @@ __global__ void __launch_bounds__(256, 1) householder_qr_crit_kernel(DevSys sy, 
     }
     for (int j = 0; j + 1 < n; ++j) {
       const int c = j + 1;
-      if (j >= 1) {
+      // column c arrives with H_0..H_{c-3} from its owner warp (U[c]); this CTA
+      // applies H_{c-2} = H_{j-1} and H_{c-1} = H_j itself (look-ahead of two:
+      // the owner warp's update of a full column is not on the chain)
+      if (j >= 2) {
         if (threadIdx.x == 0) flag_wait(fU + c, epoch);
         __syncthreads();
       }
-      const md::mdv<K> v0 = md::load_cg<K>(vhead, n, j);
-      const md::mdv<K> bt = md::load_cg<K>(beta, n, j);  // beta itself (the owner forms it)
-      double sl[K];
-      lv_zero<K>(sl);
-      for (int r = j + threadIdx.x; r < n; r += NT) {
-        const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
-        lv_prod<K>(sl, v, md::load_cg<K>(W, ls, (long long)c * n + r));
-      }
-      const md::mdv<K> dot = block_sum_levels<K>(sl, scratch);
-      const md::mdv<K> nw_ = md::neg<K>(md::mul<K>(bt, dot));
       double sg[K];
       lv_zero<K>(sg);
-      for (int r = j + threadIdx.x; r < n; r += NT) {
-        const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
-        const md::mdv<K> w = md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)c * n + r), nw_, v);
-        md::store_cg<K>(W, ls, (long long)c * n + r, w);
-        if (r > c) lv_prod<K>(sg, w, w);
-        if (r == c) md::store<K>(sx0, 1, 0, w);
+      for (int jj = (j >= 1 ? j - 1 : j); jj <= j; ++jj) {
+        const md::mdv<K> v0 = md::load_cg<K>(vhead, n, jj);
+        const md::mdv<K> bt = md::load_cg<K>(beta, n, jj);  // beta itself (the owner forms it)
+        double sl[K];
+        lv_zero<K>(sl);
+        for (int r = jj + threadIdx.x; r < n; r += NT) {
+          const md::mdv<K> v = (r == jj) ? v0 : md::load_cg<K>(W, ls, (long long)jj * n + r);
+          lv_prod<K>(sl, v, md::load_cg<K>(W, ls, (long long)c * n + r));
+        }
+        const md::mdv<K> dot = block_sum_levels<K>(sl, scratch);
+        const md::mdv<K> nw_ = md::neg<K>(md::mul<K>(bt, dot));
+        const bool last = (jj == j);
+        for (int r = jj + threadIdx.x; r < n; r += NT) {
+          const md::mdv<K> v = (r == jj) ? v0 : md::load_cg<K>(W, ls, (long long)jj * n + r);
+          const md::mdv<K> w = md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)c * n + r), nw_, v);
+          md::store_cg<K>(W, ls, (long long)c * n + r, w);
+          if (last && r >= c) lv_prod<K>(sg, w, w);  // sigma = sum_{r >= c} x_r^2
+          if (last && r == c) md::store<K>(sx0, 1, 0, w);
+        }
+        __syncthreads();  // the column's rows, written by other threads, feed the next dot
       }
-      __syncthreads();
       if (threadIdx.x == 0) flag_set(fA + c, epoch);  // rows > c final (cumulative after the barrier)
       const md::mdv<K> sig = block_sum_levels<K>(sg, scratch);
       if (threadIdx.x < 32) {
-        reflector_from_sigma<K>(n, c, sig, md::load<K>(sx0, 1, 0), W, vhead, beta, rdiag, status, true);
+        reflector_from_sigma<K>(n, c, sig, md::load<K>(sx0, 1, 0), W, vhead, beta, rdiag, status, true, ls);
         __syncwarp();
         if (lane == 0) flag_set(fB + c, epoch);
       }
@@ -507,31 +479,38 @@ __global__ void __launch_bounds__(256, 1) householder_qr_crit_kernel(DevSys sy, 
     return;
   }
   // ---------------- the column updates: warps of CTAs 1.., column c (c >= 1)
-  const int rw = (blockIdx.x - 1) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  // interleave: warp w of CTA b (b >= 1) owns columns 1 + w (G - 1) + (b - 1), ... (every SM
+  // holds columns spread over the whole range, as in householder_qr_kernel)
+  const int rw = interleave ? (int)((threadIdx.x >> 5) * (gridDim.x - 1) + blockIdx.x - 1)
+                            : (int)((blockIdx.x - 1) * (blockDim.x >> 5) + (threadIdx.x >> 5));
   const int nrw = (gridDim.x - 1) * (blockDim.x >> 5);
   for (int j = 0; j + 1 < ncol && j < n; ++j) {
-    // owned columns c > j + 1 (c = j + 1 is the critical CTA's at step j)
+    // owned columns c > j, except the chain columns c in {j+1, j+2} (c < n: H_{c-2}
+    // and H_{c-1} are the critical CTA's); the columns of I (c >= n) take every H_j
     int c0 = 1 + rw;
-    if (c0 <= j + 1) c0 += ((j + 1 - c0) / nrw + 1) * nrw;
+    if (c0 <= j) c0 += ((j - c0) / nrw + 1) * nrw;
     if (c0 >= ncol) break;
+    auto chain_col = [&](int cc) { return cc < n && cc <= j + 2; };
     if (j > 0) flag_wait(fA + j, epoch);
     __syncwarp();
     constexpr int MAXC = 4;
     md::mdv<K> part[MAXC];
     int nc = 0;
-    for (int cc = c0; cc < ncol && nc < MAXC; cc += nrw, ++nc) {  // partial dots over rows > j
+    for (int cc = c0; cc < ncol && nc < MAXC; cc += nrw) {  // partial dots over rows > j
+      if (chain_col(cc)) continue;
       double sl[K];
       lv_zero<K>(sl);
       for (int r = j + 1 + lane; r < n; r += 32)
         lv_prod<K>(sl, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)cc * n + r));
-      part[nc] = md::group_sum_levels<K>(sl, 32);
+      part[nc++] = md::group_sum_levels<K>(sl, 32);
     }
     flag_wait(fB + j, epoch);
     __syncwarp();
     const md::mdv<K> v0 = md::load_cg<K>(vhead, n, j);
     const md::mdv<K> bt = md::load_cg<K>(beta, n, j);
     int ic = 0;
-    for (int cc = c0; cc < ncol; cc += nrw, ++ic) {
+    for (int cc = c0; cc < ncol; cc += nrw) {
+      if (chain_col(cc)) continue;
       md::mdv<K> dot;
       if (ic < MAXC) {
         dot = part[ic];
@@ -542,13 +521,27 @@ __global__ void __launch_bounds__(256, 1) householder_qr_crit_kernel(DevSys sy, 
           lv_prod<K>(sl, md::load_cg<K>(W, ls, (long long)j * n + r), md::load_cg<K>(W, ls, (long long)cc * n + r));
         dot = md::group_sum_levels<K>(sl, 32);
       }
+      ++ic;
       dot = md::fma_acc<K>(dot, v0, md::load_cg<K>(W, ls, (long long)cc * n + j));
       const md::mdv<K> nw_ = md::neg<K>(md::mul<K>(bt, dot));
-      for (int r = j + lane; r < n; r += 32) {
-        const md::mdv<K> v = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
-        md::store_cg<K>(W, ls, (long long)cc * n + r, md::fma_acc<K>(md::load_cg<K>(W, ls, (long long)cc * n + r), nw_, v));
+      constexpr int QB = (K == 8) ? 2 : 4;  // rows per lane loaded together
+      for (int rb = j + lane; rb < n; rb += 32 * QB) {
+        md::mdv<K> wq[QB], vq[QB];
+#pragma unroll
+        for (int q = 0; q < QB; ++q) {
+          const int r = rb + 32 * q;
+          if (r < n) {
+            wq[q] = md::load_cg<K>(W, ls, (long long)cc * n + r);
+            vq[q] = (r == j) ? v0 : md::load_cg<K>(W, ls, (long long)j * n + r);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < QB; ++q) {
+          const int r = rb + 32 * q;
+          if (r < n) md::store_cg<K>(W, ls, (long long)cc * n + r, md::fma_acc<K>(wq[q], nw_, vq[q]));
+        }
       }
-      if (cc == j + 2 && cc < n) {  // H_0..H_{cc-2} applied: the critical CTA may take it
+      if (cc == j + 3 && cc < n) {  // H_0..H_{cc-3} applied: the critical CTA may take it
         __syncwarp();
         if (lane == 0) flag_set(fU + cc, epoch);
       }

@@ -70,6 +70,7 @@ struct ns_system {
   int qr_threads = 128;        // threads per CTA of the QR kernel
   bool qr_owner_beta = false;  // grid QR: the reflector's owner forms beta (NS_QR_OWNER_BETA)
   bool qr_small_regs = false;  // grid QR: register-light variant, 2 CTAs per SM (n > 128)
+  bool qr_interleave = true;   // grid QR: column c owned by CTA c mod grid (NS_QR_INTERLEAVE)
   bool qr_crit = false;        // grid QR with a dedicated critical-chain CTA (octo double, n <= 128)
   bool cqr_on = false;         // cluster QR (cqr.cuh) instead of householder_qr_kernel
   int cqr_P = 0, cqr_W = 0, cqr_CPC = 0, cqr_RS = 0, cqr_E = 0;

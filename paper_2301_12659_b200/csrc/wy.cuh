@@ -28,23 +28,23 @@ namespace ns {
 // the operands of WY_B consecutive terms are loaded before any is used (one L2
 // round trip per batch instead of per term), alternating between two level
 // accumulators (ILP), joined at the end in a fixed order.
-constexpr int wy_batch(int K) { return K == 8 ? 2 : 4; }
+__host__ __device__ constexpr int wy_batch(int K) { return K == 8 ? 1 : (K == 4 ? 2 : 4); }
 template <int K, class FA, class FB>
-__device__ __forceinline__ void lv_dot_strided(double (&sl)[K], int t0, int t1, FA fa, FB fb) {
+__device__ __forceinline__ void lv_dot_strided(double (&sl)[K], int t0, int t1, FA fa, FB fb, int stride = 32) {
   constexpr int B = wy_batch(K);
   double s1[K];
   lv_zero<K>(s1);
-  for (int t = t0; t < t1; t += 32 * B) {
+  for (int t = t0; t < t1; t += stride * B) {
     md::mdv<K> a[B], b[B];
 #pragma unroll
     for (int q = 0; q < B; ++q)
-      if (t + 32 * q < t1) {
-        a[q] = fa(t + 32 * q);
-        b[q] = fb(t + 32 * q);
+      if (t + stride * q < t1) {
+        a[q] = fa(t + stride * q);
+        b[q] = fb(t + stride * q);
       }
 #pragma unroll
     for (int q = 0; q < B; ++q)
-      if (t + 32 * q < t1) {
+      if (t + stride * q < t1) {
         if (q & 1) lv_prod<K>(s1, a[q], b[q]);
         else lv_prod<K>(sl, a[q], b[q]);
       }
@@ -187,6 +187,7 @@ struct WyArgs {
 
 template <int K>
 __global__ void __launch_bounds__(256) stage_wy_kernel(DevSys s, WyArgs a, unsigned* bar) {
+  __shared__ double red[K * 9];  // block_sum_levels scratch (8 warps + result)
   GridBarrier gb(bar, 0u);
   const int n = s.n, d = s.d, BW = a.BW, P = a.P;
   const int gw = gwarp(), nw = nwarps(), lane = lane_id();
@@ -199,16 +200,19 @@ __global__ void __launch_bounds__(256) stage_wy_kernel(DevSys s, WyArgs a, unsig
     // ---- y = Q^T b'_k, block by block
     for (int p = 0; p < P; ++p) {
       const int j0 = p * BW, nbw = min(BW, n - j0);
-      for (int l = gw; l < nbw; l += nw) {  // u_l = v_{j0+l}^T y: one warp per reflector
+      // u_l = v_{j0+l}^T y: one CTA per reflector, its threads split the rows (a
+      // warp alone on a 1024-row dot waited ~240 cycles per term on its SMSP's
+      // share of the FP64 pipe)
+      for (int l = blockIdx.x; l < nbw; l += gridDim.x) {
         const int j = j0 + l;
         double s0[K];
         lv_zero<K>(s0);
-        if (lane == 0) lv_prod<K>(s0, md::load<K>(a.vh, n, j), md::load_cg<K>(a.y, n, j));
+        if (threadIdx.x == 0) lv_prod<K>(s0, md::load<K>(a.vh, n, j), md::load_cg<K>(a.y, n, j));
         lv_dot_strided<K>(
-            s0, j + 1 + lane, n, [&](int r) { return md::load<K>(a.W, nn, (long long)j * n + r); },
-            [&](int r) { return md::load_cg<K>(a.y, n, r); });
-        const md::mdv<K> t = md::group_sum_levels<K>(s0, 32);
-        if (lane == 0) md::store_cg<K>(a.up, BW, l, t);
+            s0, j + 1 + threadIdx.x, n, [&](int r) { return md::load<K>(a.W, nn, (long long)j * n + r); },
+            [&](int r) { return md::load_cg<K>(a.y, n, r); }, blockDim.x);
+        const md::mdv<K> t = block_sum_levels<K>(s0, red);
+        if (threadIdx.x == 0) md::store_cg<K>(a.up, BW, l, t);
       }
       gb.sync();
       for (int i = gw; i < nbw; i += nw) {  // u'_i = sum_{l <= i} T[l][i] u_l
@@ -237,14 +241,14 @@ __global__ void __launch_bounds__(256) stage_wy_kernel(DevSys s, WyArgs a, unsig
     for (int t = P - 1; t >= 0; --t) {
       const int t0 = t * BW, t1 = min(n, t0 + BW);
       if (t < P - 1) {  // z_r = y_r - sum_{c >= t1} R[r][c] dx_k[c]  (z kept in y)
-        for (int r = t0 + gw; r < t1; r += nw) {
+        for (int r = t0 + blockIdx.x; r < t1; r += gridDim.x) {  // one CTA per row
           double sl[K];
           lv_zero<K>(sl);
           lv_dot_strided<K>(
-              sl, t1 + lane, n, [&](int c) { return md::load<K>(a.R, nn, (long long)r * n + c); },
-              [&](int c) { return md::load_cg<K>(dxk, lsV, c); });
-          const md::mdv<K> acc = md::group_sum_levels<K>(sl, 32);
-          if (lane == 0) md::store_cg<K>(a.y, n, r, md::sub<K>(md::load_cg<K>(a.y, n, r), acc));
+              sl, t1 + threadIdx.x, n, [&](int c) { return md::load<K>(a.R, nn, (long long)r * n + c); },
+              [&](int c) { return md::load_cg<K>(dxk, lsV, c); }, blockDim.x);
+          const md::mdv<K> acc = block_sum_levels<K>(sl, red);
+          if (threadIdx.x == 0) md::store_cg<K>(a.y, n, r, md::sub<K>(md::load_cg<K>(a.y, n, r), acc));
         }
         gb.sync();
       }

@@ -4,6 +4,8 @@ from __future__ import annotations
 
 from fractions import Fraction
 
+import math
+
 import numpy as np
 
 import synth
@@ -32,7 +34,10 @@ def to_frac(F, v) -> Fraction:
 def err_ratio(gpu_limbs, oracle_val, F, scale: float) -> float:
     """|gpu - oracle| / scale as a float (scale > 0).  mp fields: the limbs
     summed exactly in the field's precision (>= 2x the md bits, so the sum of
-    K nonoverlapping doubles is exact), the difference in the field."""
+    K nonoverlapping doubles is exact), the difference in the field.  A
+    non-finite GPU limb is an infinite error (max() would drop a NaN ratio)."""
+    if not all(math.isfinite(float(l)) for l in gpu_limbs):
+        return float("inf")
     if hasattr(F, "ctx") and not getattr(F, "is_complex", False):
         c = F.ctx
         g = c.fsum([c.mpf(float(l)) for l in gpu_limbs])

@@ -479,6 +479,18 @@ def test_wy_solve_path_n300_banded():
     _full_parity(sys_, x, F, out=out, nonvacuous=True)
 
 
+@pytest.mark.parametrize("K,env", [(8, dict(NS_QR_CRIT=1)), (4, dict(NS_QR_CRIT=1, NS_WY=1, NS_WY_BW=16)),
+                                   (4, dict(NS_QR_INTERLEAVE=0)), (4, dict(NS_QR_INTERLEAVE=0, NS_WY=1))])
+def test_grid_qr_variants(K, env):
+    """The grid-QR variants: a dedicated critical-chain CTA (NS_QR_CRIT) on
+    [A0 | I] and on A0 alone (the WY path), and the contiguous column ownership
+    (NS_QR_INTERLEAVE=0) of both: full oracle parity on 'rough' input."""
+    sys_ = synth.triangular_system(40, 12, K, seed=53)
+    x = synth.make_x(sys_, "rough", seed=54)
+    with _env(**env):
+        _full_parity(sys_, x, O.field_for(K), nonvacuous=True)
+
+
 @pytest.mark.parametrize("owner", [0, 1])
 def test_grid_qr_owner_beta_modes(owner):
     """NS_QR_OWNER_BETA: the reflector's owner forms beta (1, default) or each
