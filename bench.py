@@ -30,6 +30,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+
+# single-threaded BLAS (the oracle's pools + OpenBLAS threads deadlocked a test process)
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 import subprocess
 import sys
 import threading

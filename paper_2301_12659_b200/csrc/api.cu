@@ -141,7 +141,7 @@ void free_all(ns_system* s) {
                   s->invR, s->bp, s->dx, s->y, s->part, s->Minv, s->Z, s->pend, s->sflags, s->rbuf, s->knorm, s->res_tmp, s->ws, s->job_counter,
                   s->bar, s->status, s->bws, s->A0q, s->qr_flags, s->jobs, s->ser_off, s->pool, s->prog, s->left,
                   s->left_init, s->trace, s->strace, s->sample_rows, s->bpart, s->strace_b,
-                  s->wy_blk, s->wy_X, s->wy_T1, s->wy_up, s->wy_u};
+                  s->wy_blk, s->wy_X, s->wy_T1, s->wy_up, s->wy_u, s->Vr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& row : s->ev)
@@ -270,6 +270,13 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
     const int bw = atoi(e);
     if (bw >= 2 && bw <= 256 && (bw & (bw - 1)) == 0) s->wy_BW = bw;
   }
+  // n <= 256 (no cluster QR: see setup): QR of A_0 alone and Q^T from one WY block (NS_WYM)
+  s->wym = !s->wy && n <= 256;
+  if (const char* e = getenv("NS_WYM")) s->wym = !s->wy && n <= 256 && atoi(e) != 0;
+  if (s->wym) {
+    s->wy_BW = 2;
+    while (s->wy_BW < n) s->wy_BW *= 2;
+  }
   s->wy_P = (n + s->wy_BW - 1) / s->wy_BW;
   const int L = desc->mono_ptr[M];
   s->h_eq_ptr.assign(desc->eq_ptr, desc->eq_ptr + n + 1);
@@ -358,7 +365,8 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
     s->cmax = std::max(1, (std::max(1, (int)d - 1) * maxlen + 63) / 64);  // ns::UCH = 64
     ok &= dalloc(&s->part, (size_t)K * n * s->cmax) == cudaSuccess;
   }
-  if (s->wy) {
+  if (s->wy || s->wym) {
+    ok &= dalloc(&s->Vr, (size_t)K * nn) == cudaSuccess;
     const size_t nb = (size_t)K * 2 * s->wy_P * s->wy_BW * s->wy_BW;
     ok &= dalloc(&s->wy_blk, nb) == cudaSuccess;
     ok &= dalloc(&s->wy_X, nb) == cudaSuccess;

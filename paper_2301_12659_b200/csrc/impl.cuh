@@ -54,7 +54,7 @@ ns_status launch_wy_factors(ns_system* s, cudaStream_t st) {
   const int n = s->n, BW = s->wy_BW, P = s->wy_P;
   const long long nn = (long long)n * n;
   const int ub = (int)std::min<long long>((nn + 255) / 256, 4LL * s->sms);
-  ns::wy_unpack_kernel<K><<<ub, 256, 0, st>>>(n, BW, P, s->W, s->vhead, s->R, s->Minv, s->wy_blk);
+  ns::wy_unpack_kernel<K><<<ub, 256, 0, st>>>(n, BW, P, s->W, s->vhead, s->R, s->Vr, s->wy_blk);
   const long long tasks = (long long)P * BW * BW;
   const int gb = (int)std::min<long long>((tasks + 7) / 8, 8LL * s->sms);
   ns::wy_gram_kernel<K><<<gb, 256, 0, st>>>(n, BW, P, s->W, s->vhead, s->beta, s->qr_owner_beta ? 1 : 0, s->wy_blk);
@@ -64,8 +64,17 @@ ns_status launch_wy_factors(ns_system* s, cudaStream_t st) {
   double *X = s->wy_X, *T1 = s->wy_T1;
   unsigned* bar2 = s->bar + 4;
   void* args[] = {&nblk, (void*)&BW, (void*)&S, &X, &T1, &bar2};
-  CK(cudaLaunchCooperativeKernel((const void*)ns::invert_upper_kernel<K>, dim3(s->sms), dim3(256), args, 0, st));
+  // wym (n <= 256) runs beside eval/diff: a small cooperative grid that fits
+  const int ig = s->wy ? s->sms : std::min(s->sms, 16);
+  CK(cudaLaunchCooperativeKernel((const void*)ns::invert_upper_kernel<K>, dim3(ig), dim3(256), args, 0, st));
   s->last_launches += 4;
+  if (s->wym) {  // Q^T = I - V (T^T V^T), row-major, for form_m
+    const long long lsX = 2LL * P * BW * BW;
+    const int zb = (int)std::min<long long>((nn * 8 / 32 + 7) / 8 + 1, 4LL * s->sms);
+    ns::wy_z_kernel<K><<<zb, 256, 0, st>>>(n, BW, s->wy_X, lsX, s->Vr, s->Z);
+    ns::wy_qt_kernel<K><<<zb, 256, 0, st>>>(n, s->Vr, s->Z, s->Qt);
+    s->last_launches += 2;
+  }
   CK(cudaGetLastError());
   s->qr_cached = true;
   return NS_OK;
@@ -111,7 +120,7 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
     s->last_launches += 1;
   } else {
     int ob = s->qr_owner_beta ? 1 : 0;
-    int ncol = s->wy ? n : 2 * n;
+    int ncol = (s->wy || s->wym) ? n : 2 * n;
     int il = s->qr_interleave ? 1 : 0;
     void* args[] = {&ds, (void*)&xp, &n, (void*)&A0, &W, &vh, &be, &rd, &bar, &stt, &fl, &epoch, &ob, &ncol, &il};
     if (s->qr_crit) {
@@ -124,11 +133,16 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
       CK(cudaLaunchCooperativeKernel(qk, dim3(s->grid_qr), dim3(s->qr_threads), args, s->qr_smem_reserve, st));
     }
     s->qr_epoch = epoch;
-    if (s->wy) return launch_wy_factors<K>(s, st);
-    const long long tot = (long long)K * n * n;
-    const int blocks = (int)std::min<long long>((tot + 255) / 256, 4LL * s->sms);
-    ns::qr_unpack_kernel<K><<<blocks, 256, 0, st>>>(n, s->W, s->R, s->Qt);
-    s->last_launches += 2;
+    if (s->wy || s->wym) {
+      const ns_status r = launch_wy_factors<K>(s, st);
+      if (r || s->wy) return r;
+    } else {
+      const long long tot = (long long)K * n * n;
+      const int blocks = (int)std::min<long long>((tot + 255) / 256, 4LL * s->sms);
+      ns::qr_unpack_kernel<K><<<blocks, 256, 0, st>>>(n, s->W, s->R, s->Qt);
+      s->last_launches += 1;
+    }
+    s->last_launches += 1;
   }
   const bool m_done = s->cqr_on && s->cqr_withM && s->use_m;  // M formed inside the cluster QR
   if (!m_done) {
@@ -145,7 +159,10 @@ ns_status launch_qr(ns_system* s, const double* A0src, const double* x, cudaStre
     void* margs[] = {&n, &TB, (void*)&R, (void*)&Qt, (void*)&iR, &M, &Z, &bar2};
     // 8 warps per SM: the md chains are dependent DADD sequences, one warp per
     // SMSP left the FP64 pipe 90% idle (ncu, C3)
-    CK(cudaLaunchCooperativeKernel((const void*)ns::form_m_kernel<K>, dim3(s->grid_st), dim3(256), margs, 0, st));
+    // wym: on the QR's own SMs (freed when the QR ends), so that M forms beside the
+    // still-running eval/diff instead of waiting for a whole-GPU co-resident grid
+    const int fg = s->wym ? std::min(s->grid_st, std::max(1, s->grid_qr)) : s->grid_st;
+    CK(cudaLaunchCooperativeKernel((const void*)ns::form_m_kernel<K>, dim3(fg), dim3(256), margs, 0, st));
     s->last_launches += 1;
   }
   CK(cudaGetLastError());
@@ -158,7 +175,7 @@ ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
   if (s->wy) {
     CK(cudaMemsetAsync(s->bar + 2, 0, 2 * sizeof(unsigned), st));
     DevSys ds = devsys(s);
-    ns::WyArgs a{s->b, s->A, s->W, s->Minv, s->vhead, s->R, s->wy_X, s->bp, s->dx, s->y, s->part, s->wy_up, s->wy_u,
+    ns::WyArgs a{s->b, s->A, s->W, s->Vr, s->vhead, s->R, s->wy_X, s->bp, s->dx, s->y, s->part, s->wy_up, s->wy_u,
                  s->cmax, s->wy_BW, s->wy_P, k_lo};
     unsigned* bar = s->bar + 2;
     void* args[] = {&ds, &a, &bar};
@@ -231,7 +248,8 @@ ns_status setup_grids(ns_system* s) {
   // larger systems use 8 warps per CTA (the column updates are throughput work)
   // 8 warps per CTA: the grid QR then holds half as many SMs (reserved, below),
   // leaving them to the concurrent eval/diff (C3: 10.25 vs 10.99 ms per step)
-  s->qr_threads = 256;
+  // wym (A_0 alone, n <= 256): 4 warps per CTA, one column-owner warp per SMSP
+  s->qr_threads = s->wym ? 128 : 256;
   if (const char* e = getenv("NS_QR_THREADS")) s->qr_threads = atoi(e) >= 256 ? 256 : 128;
   // the owner forms beta once: at 8 warps per CTA the per-consumer reciprocals
   // competed with the owner's chain for the FP64 pipes (C3 QR 7.03 -> 6.92 ms, C4 66.8 -> 63.4)
@@ -245,7 +263,7 @@ ns_status setup_grids(ns_system* s) {
   s->qr_interleave = s->wy;
   if (const char* e = getenv("NS_QR_INTERLEAVE")) s->qr_interleave = atoi(e) != 0;
   if (const char* e = getenv("NS_QR_SMALLREGS")) s->qr_small_regs = atoi(e) != 0;
-  const int qcols = s->wy ? s->n : 2 * s->n;  // columns of the factored matrix
+  const int qcols = (s->wy || s->wym) ? s->n : 2 * s->n;  // columns of the factored matrix
   s->grid_qr = std::min(s->sms * (s->qr_small_regs ? 2 : 1),
                         std::max(1, (qcols + s->qr_threads / 32 - 1) / (s->qr_threads / 32)));
   // a dedicated CTA for the dependent reflector chain (householder_qr_crit_kernel)
@@ -379,7 +397,7 @@ ns_status setup_grids(ns_system* s) {
   }
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ns::stage_kernel<K>, s->st_threads, 0));
   if (occ < 1) return NS_ECUDA;
-  if (s->wy) {  // cooperative grids of one CTA per SM (256 threads)
+  if (s->wy || s->wym) {  // cooperative grids of one CTA per SM (256 threads)
     int o1 = 0, o2 = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, ns::stage_wy_kernel<K>, 256, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, ns::invert_upper_kernel<K>, 256, 0));

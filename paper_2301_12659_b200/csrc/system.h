@@ -45,6 +45,8 @@ struct ns_system {
   // blocked WY solve (wy.cuh; n > 256 by default, NS_WY overrides): QR of A_0 alone,
   // T_p of BW-reflector blocks, per-stage Q^T b by blocks; V (row-major) lives in Minv
   bool wy = false;
+  bool wym = false;            // n <= 256 without the cluster QR: A_0 alone, Q^T = I - V T^T V^T, then M
+  double* Vr = nullptr;        // [K][n][n] V row-major (wy / wym)
   int wy_BW = 256, wy_P = 0;
   double *wy_blk = nullptr, *wy_X = nullptr, *wy_T1 = nullptr, *wy_up = nullptr, *wy_u = nullptr;
   int cmax = 1;

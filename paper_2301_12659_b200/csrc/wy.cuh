@@ -268,3 +268,61 @@ __global__ void __launch_bounds__(256) stage_wy_kernel(DevSys s, WyArgs a, unsig
 }
 
 }  // namespace ns
+
+namespace ns {
+
+// ---------------------------------------------------------------- Q^T from one WY block
+// n <= 256 without the cluster QR (C3): the QR factors A_0 alone (n columns, not
+// the 2n of [A_0 | I]: half the column updates on the reflector chain), then
+// Q^T = I - V T^T V^T (one block, BW >= n) is formed by two parallel products and
+// M = R^{-1} Q^T by form_m_kernel as before.  Lane groups of WY_G lanes per output
+// entry (lane s sums the terms s, s + WY_G, ... as level sums, then a butterfly).
+constexpr int WY_G = 8;
+
+// Z = T^T V^T:  Z[l][c] = sum_{i <= min(l, c)} T[i][l] V[c][i]  (row-major n x n)
+template <int K>
+__global__ void __launch_bounds__(256) wy_z_kernel(int n, int BW, const double* __restrict__ X, long long lsX,
+                                                   const double* __restrict__ V, double* Z) {
+  const long long nn = (long long)n * n;
+  const int lane = threadIdx.x & 31, sub = lane % WY_G;
+  constexpr int OPW = 32 / WY_G;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long base = gw * OPW; base < nn; base += nw * OPW) {
+    const long long o = base + lane / WY_G;
+    const bool ok = o < nn;
+    const int l = ok ? (int)(o / n) : 0, c = ok ? (int)(o % n) : 0;
+    double sl[K];
+    lv_zero<K>(sl);
+    if (ok)
+      for (int i = sub; i <= min(l, c); i += WY_G)
+        lv_prod<K>(sl, md::load<K>(X, lsX, (long long)i * BW + l), md::load<K>(V, nn, (long long)c * n + i));
+    const md::mdv<K> z = md::group_sum_levels<K>(sl, WY_G);
+    if (ok && sub == 0) md::store<K>(Z, nn, o, z);
+  }
+}
+
+// Q^T = I - V Z:  Qt[r][c] = delta_rc - sum_{l <= r} V[r][l] Z[l][c]  (row-major n x n)
+template <int K>
+__global__ void __launch_bounds__(256) wy_qt_kernel(int n, const double* __restrict__ V, const double* __restrict__ Z,
+                                                    double* Qt) {
+  const long long nn = (long long)n * n;
+  const int lane = threadIdx.x & 31, sub = lane % WY_G;
+  constexpr int OPW = 32 / WY_G;
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long base = gw * OPW; base < nn; base += nw * OPW) {
+    const long long o = base + lane / WY_G;
+    const bool ok = o < nn;
+    const int r = ok ? (int)(o / n) : 0, c = ok ? (int)(o % n) : 0;
+    double sl[K];
+    lv_zero<K>(sl);
+    if (ok)
+      for (int l = sub; l <= r; l += WY_G)
+        lv_prod<K>(sl, md::load<K>(V, nn, (long long)r * n + l), md::load<K>(Z, nn, (long long)l * n + c));
+    const md::mdv<K> t = md::group_sum_levels<K>(sl, WY_G);
+    if (ok && sub == 0) md::store<K>(Qt, nn, o, md::sub<K>(md::from_double<K>(r == c ? 1.0 : 0.0), t));
+  }
+}
+
+}  // namespace ns

@@ -1,6 +1,12 @@
 import os
 import sys
 
+# single-threaded BLAS in the test process: after the oracle's worker pools,
+# OpenBLAS's threaded inverse of the 128 x 128 A_0 (stage_scales) deadlocked the
+# process and hung the C3 full-parity tests (a fresh process inverts it in 1 ms)
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

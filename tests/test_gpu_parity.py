@@ -491,6 +491,34 @@ def test_grid_qr_variants(K, env):
         _full_parity(sys_, x, O.field_for(K), nonvacuous=True)
 
 
+@pytest.mark.parametrize("K,env", [(8, dict(NS_WYM=0)), (8, dict(NS_WYM=1)), (4, dict(NS_CQR=0, NS_WYM=1)),
+                                   (4, dict(NS_CQR=0, NS_WYM=0)), (2, dict(NS_CQR=0, NS_WYM=1, NS_TILED_BS_ENV=1))])
+def test_qr_of_a0_alone_and_qt_from_wy(K, env):
+    """n <= 256 without the cluster QR: the QR of A_0 alone with Q^T = I - V T^T V^T
+    formed from one WY block (NS_WYM=1, the default) against [A_0 | I] (NS_WYM=0);
+    full oracle parity on 'rough' input (also the tiled back substitution on Q^T)."""
+    import paper_2301_12659_b200 as P
+    torch = _torch()
+    sys_ = synth.triangular_system(40, 7 if K == 2 else 12, K, seed=55)
+    x = synth.make_x(sys_, "rough", seed=56)
+    F = O.field_for(K)
+    env = dict(env)
+    tiled = env.pop("NS_TILED_BS_ENV", 0)
+    with _env(**env):
+        if not tiled:
+            _full_parity(sys_, x, F, nonvacuous=True)
+            return
+        out = H.step_oracle(sys_, x, F)
+        sc = O.scales(sys_, x)
+        n, d = sys_.n, sys_.d
+        dxf = np.array([[float(out["dx"][k][i]) for i in range(n)] for k in range(d)])
+        s_k, _ = O.stage_scales(sys_, x, H.dense_A0_float(out["A"], n), dxf, sc["s_b"], sc["s_A"])
+        h = _handle(sys_)
+        xt = torch.tensor(x, device="cuda:0")
+        h.step(xt, flags=P.NS_TILED_BS)
+        assert H.xnew_errors(sys_, x, out, _np(xt), F, s_k) <= 1
+
+
 @pytest.mark.parametrize("owner", [0, 1])
 def test_grid_qr_owner_beta_modes(owner):
     """NS_QR_OWNER_BETA: the reflector's owner forms beta (1, default) or each
