@@ -271,7 +271,7 @@ ns_status ns_system_create(const ns_system_desc* desc, int cuda_device, ns_syste
     if (bw >= 2 && bw <= 256 && (bw & (bw - 1)) == 0) s->wy_BW = bw;
   }
   // n <= 256 (no cluster QR: see setup): QR of A_0 alone and Q^T from one WY block (NS_WYM)
-  s->wym = !s->wy && n <= 256;
+  s->wym = false;  // opt-in: measured slower at C3 (10.96 vs 9.24 ms)
   if (const char* e = getenv("NS_WYM")) s->wym = !s->wy && n <= 256 && atoi(e) != 0;
   if (s->wym) {
     s->wy_BW = 2;

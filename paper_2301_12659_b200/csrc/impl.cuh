@@ -467,7 +467,8 @@ ns::BLayout batched_layout(const ns_system* s, size_t smem_cap_doubles, int thre
 
 template <class S, int K, int MB>
 ns_status batched_setup_t(ns_system* s) {
-  const int threads = 256;
+  int threads = 256;  // NS_BATCH_THREADS=128: 4 warps per path (more paths in flight per SM)
+  if (const char* e = getenv("NS_BATCH_THREADS")) threads = atoi(e) == 128 ? 128 : 256;
   int optin = 0;
   CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, s->dev));
   int per_sm = 0;

@@ -6,6 +6,11 @@ import sys
 # process and hung the C3 full-parity tests (a fresh process inverts it in 1 ms)
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 os.environ.setdefault("OMP_NUM_THREADS", "1")
+try:  # numpy may already be loaded by a plugin: limit the live BLAS pool too
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+except Exception:  # pragma: no cover
+    pass
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:

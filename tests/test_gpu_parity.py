@@ -56,10 +56,12 @@ def _run_all(sys_, x_np):
                 rdiag=_np(rdiag), status=st.status_bits, pattern=h.pattern())
 
 
-def _full_parity(sys_, x_np, F, eps_cap=64.0, out=None, nonvacuous=False):
+def _full_parity(sys_, x_np, F, eps_cap=64.0, out=None, nonvacuous=False, nonvacuous_k=None):
     """The whole step against the oracle (out: its result, computed here if
-    None).  nonvacuous: assert tol_p s_k < max_i |dx_k,i| at every k, i.e. a
-    wrong dx_k (even dx_k = 0) would fail the tolerance."""
+    None).  nonvacuous: assert tol_p s_k < max_i |dx_k,i| at every k < nonvacuous_k
+    (default: every k), i.e. a wrong dx_k (even dx_k = 0) would fail the
+    tolerance; beyond it the late-coefficient condition kappa_k makes
+    any check at tol_p s_k vacuous (DESIGN 8)."""
     g = _run_all(sys_, x_np)
     if out is None:
         out = H.step_oracle(sys_, x_np, F)
@@ -78,10 +80,10 @@ def _full_parity(sys_, x_np, F, eps_cap=64.0, out=None, nonvacuous=False):
     sv = H.solve_errors(sys_, x_np, out, g["dx"], F)
     print(f"\n{sys_.name} n={n} d={d} K={K}: max err/(tol s) dx {sv['dx']:.2e}; per-k max err/(eps_p |x_k|): "
           + " ".join(f"{v:.1e}" for v in sv["per_k_eps_x"]))
-    if nonvacuous:
-        vac = H.vacuity(out, sv["s"], synth.TOL_P[K])
-        assert max(vac) < 1.0, ("vacuous check at k =", [k for k, v in enumerate(vac) if v >= 1], vac)
     assert sv["dx"] <= 1, sv["dx"]
+    if nonvacuous:
+        vac = H.vacuity(out, sv["s"], synth.TOL_P[K])[:nonvacuous_k]
+        assert max(vac) < 1.0, ("vacuous check at k =", [k for k, v in enumerate(vac) if v >= 1], vac)
     assert sv["dx_eps"] <= eps_cap * n, sv["dx_eps"]
     xe = H.xnew_errors(sys_, x_np, out, g["x_new"], F, sv["s"])
     assert xe <= 1, xe
@@ -315,7 +317,8 @@ def test_C3_full_parity_rough():
     sys_ = synth.build_config("C3")
     x = synth.make_x(sys_, "rough", seed=1)
     F = O.field_for(8)
-    _full_parity(sys_, x, F, out=H.parallel_step(sys_, x, F), nonvacuous=True)
+    # 'rough' at degree 63: kappa_k ~ 1e4 per k pushes tol_p s_k above |dx_k| from k = 31 on
+    _full_parity(sys_, x, F, out=H.parallel_step(sys_, x, F), nonvacuous=True, nonvacuous_k=31)
 
 
 @pytest.mark.slow
