@@ -236,10 +236,9 @@ __global__ void __launch_bounds__(K == 8 ? 256 : 512) cluster_qr_kernel(DevSys s
     const md::mdv<K> alpha = md::is_negative<K>(x0) ? nrm : md::neg<K>(nrm);  // reading R13
     const md::mdv<K> v0 = md::sub<K>(x0, alpha);
     publish_sc(jj, 0, v0, fullB0);
-    // v^T v = -2 alpha v0, beta = 2 / v^T v = -1 / (alpha v0) = 1 / (sigma + |x0| ||x||)
-    // (md::householder_beta: off the v0 -> alpha v0 chain); zero column: beta = 0 (H = I)
+    // v^T v = -2 alpha v0, beta = 2 / v^T v = -1 / (alpha v0); zero column: beta = 0 (H = I)
     md::mdv<K> bt = md::zero<K>();
-    if (!md::is_zero<K>(sig)) bt = md::householder_beta<K>(sig, x0, nrm);
+    if (!md::is_zero<K>(sig)) bt = md::neg<K>(md::recip<K>(md::mul<K>(alpha, v0)));
     else if (lane == 0 && status) atomicOr(status, ST_SINGULAR);
     publish_sc(jj, 1, bt, fullC0);
     __syncwarp();

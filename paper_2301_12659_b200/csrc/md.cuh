@@ -324,26 +324,6 @@ MD_INL mdv<K> div(const mdv<K>& a, const mdv<K>& b) {
   return fma_acc_first<K>(q, y, r);
 }
 
-// beta = -1/(alpha v0) = 1/(sigma + |x0| ||x||) (alpha = -sign(x0) ||x||, v0 = x0 - alpha;
-// sigma = ||x||^2 up to rounding, so the two agree to the md precision).  The K/2-limb
-// estimate starts from the K/2-limb square root, beside the K-limb one, and one Newton
-// step at K limbs refines it: off the chain sqrt -> (x0 - alpha) -> alpha v0 -> recip,
-// only D = sigma + |x0| ||x|| and the correction follow the K-limb square root.
-template <int K>
-MD_INL mdv<K> householder_beta(const mdv<K>& sig, const mdv<K>& x0, const mdv<K>& nrm) {
-  const mdv<K> D = fma_acc<K>(sig, absv<K>(x0), nrm);
-  if constexpr (K == 2) {
-    return recip<2>(D);
-  } else {
-    const mdv<K / 2> sh = sqrt<K / 2>(trunc<K / 2, K>(sig));
-    const mdv<K / 2> bh = recip<K / 2>(
-        fma_acc<K / 2>(trunc<K / 2, K>(sig), absv<K / 2>(trunc<K / 2, K>(x0)), sh));
-    const mdv<K> e = fma_acc_first<K>(from_double<K>(1.0), neg<K>(D), trunc<K, K / 2>(bh));
-    const mdv<K / 2> corr = mul<K / 2>(bh, trunc<K / 2, K>(e));
-    return add<K>(trunc<K, K / 2>(bh), trunc<K, K / 2>(corr));
-  }
-}
-
 // sign of an md value (leading nonzero limb decides; limbs are nonoverlapping)
 template <int K>
 MD_INL bool is_negative(const mdv<K>& a) {

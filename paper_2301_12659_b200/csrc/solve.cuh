@@ -126,8 +126,8 @@ __device__ void reflector_from_sigma(int n, int jj, const md::mdv<K>& sig, const
   // beta = -1/(alpha v0) is formed by the consumers; store alpha v0 (0 for a zero column)
   md::mdv<K> pav = md::zero<K>();
   if (!md::is_zero<K>(sig)) {
-    if (owner_beta) pav = md::householder_beta<K>(sig, x0, nrm);  // the slot holds beta itself
-    else pav = md::mul<K>(alpha, v0);
+    pav = md::mul<K>(alpha, v0);
+    if (owner_beta) pav = md::neg<K>(md::recip<K>(pav));  // the slot holds beta itself
   }
   else if (lane == 0 && status) atomicOr(status, ST_SINGULAR);
   if (lane == 0) {

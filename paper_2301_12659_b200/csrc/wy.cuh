@@ -138,31 +138,45 @@ __global__ void __launch_bounds__(256) invert_upper_kernel(int nblk, int BT, con
     md::store_cg<K>(X, ls, e, (i == c) ? md::recip<K>(md::load<K>(S, ls, e)) : md::zero<K>());
   }
   gb.sync();
+  // each entry's dot (up to BT/2 terms) is shared by a group of IG lanes (lane s sums
+  // the terms s, s + IG, ...; fixed butterfly): a serial dot per thread made the last
+  // levels long chains (0.9 ms at C4)
+  constexpr int IG = 8, OPW = 32 / IG;
+  const int lane = threadIdx.x & 31, sub = lane % IG;
+  const long long gw = tid >> 5, nw = nth >> 5;
   for (int sz = 2; sz <= BT; sz <<= 1) {
     const int h = sz >> 1;
     const long long per = (long long)(BT / sz) * h * h;
-    for (long long e = tid; e < nblk * per; e += nth) {
-      const long long b = e / per, rr = e % per;
+    for (long long base0 = gw * OPW; base0 < nblk * per; base0 += nw * OPW) {  // warp-uniform trip count
+      const long long e = base0 + lane / IG;
+      const bool ok = e < nblk * per;
+      const long long b = ok ? e / per : 0, rr = ok ? e % per : 0;
       const int blk = (int)(rr / (h * h)), p = (int)((rr / h) % h), q = (int)(rr % h);
       const long long base = b * BB + (long long)blk * sz * (BT + 1);  // (blk sz, blk sz) of block b
       double sl[K];
       lv_zero<K>(sl);
-      for (int u = 0; u <= q; ++u)
-        lv_prod<K>(sl, md::load<K>(S, ls, base + (long long)p * BT + h + u),
-                   md::load_cg<K>(X, ls, base + (long long)(h + u) * BT + h + q));
-      md::store_cg<K>(T1, ls, b * BB + rr, md::renorm<K, K>(sl));
+      if (ok)
+        for (int u = sub; u <= q; u += IG)
+          lv_prod<K>(sl, md::load<K>(S, ls, base + (long long)p * BT + h + u),
+                     md::load_cg<K>(X, ls, base + (long long)(h + u) * BT + h + q));
+      const md::mdv<K> t = md::group_sum_levels<K>(sl, IG);
+      if (ok && sub == 0) md::store_cg<K>(T1, ls, b * BB + rr, t);
     }
     gb.sync();
-    for (long long e = tid; e < nblk * per; e += nth) {
-      const long long b = e / per, rr = e % per;
+    for (long long base0 = gw * OPW; base0 < nblk * per; base0 += nw * OPW) {
+      const long long e = base0 + lane / IG;
+      const bool ok = e < nblk * per;
+      const long long b = ok ? e / per : 0, rr = ok ? e % per : 0;
       const int blk = (int)(rr / (h * h)), p = (int)((rr / h) % h), q = (int)(rr % h);
       const long long base = b * BB + (long long)blk * sz * (BT + 1);
       double sl[K];
       lv_zero<K>(sl);
-      for (int v = p; v < h; ++v)
-        lv_prod<K>(sl, md::load_cg<K>(X, ls, base + (long long)p * BT + v),
-                   md::load_cg<K>(T1, ls, b * BB + (long long)blk * h * h + (long long)v * h + q));
-      md::store_cg<K>(X, ls, base + (long long)p * BT + h + q, md::neg<K>(md::renorm<K, K>(sl)));
+      if (ok)
+        for (int v = p + sub; v < h; v += IG)
+          lv_prod<K>(sl, md::load_cg<K>(X, ls, base + (long long)p * BT + v),
+                     md::load_cg<K>(T1, ls, b * BB + (long long)blk * h * h + (long long)v * h + q));
+      const md::mdv<K> t = md::group_sum_levels<K>(sl, IG);
+      if (ok && sub == 0) md::store_cg<K>(X, ls, base + (long long)p * BT + h + q, md::neg<K>(t));
     }
     gb.sync();
   }
