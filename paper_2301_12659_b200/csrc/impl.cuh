@@ -183,7 +183,7 @@ ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
     s->last_launches += 1;
     return NS_OK;
   }
-  const int wpb2 = s->st2_threads / 32;
+  const int wpb2 = s->st2_cwpb;
   const int Q = (s->n + wpb2 - 1) / wpb2;
   if (s->use_m && s->stage_split && Q <= s->grid_st2 / 2 && s->dc - k_lo >= 3) {
     // split design: critical group + right-looking bulk updates
@@ -191,7 +191,7 @@ ns_status launch_stage(ns_system* s, int k_lo, cudaStream_t st) {
     CK(cudaMemsetAsync(s->sflags, 0, sizeof(int) * (2 * s->d + 2), st));
     DevSys ds = devsys(s);
     ns::Stage2Args a{s->b, s->A, s->Minv, s->bp, s->dx, s->pend, s->sflags, s->sflags + s->d,
-                     (unsigned*)(s->sflags + 2 * s->d), Q, k_lo, s->strace, s->bpart};  // sflags[0]: dx published counter
+                     (unsigned*)(s->sflags + 2 * s->d), Q, k_lo, s->strace, s->bpart, wpb2};  // sflags[0]: dx published counter
     unsigned* bar = s->bar + 2;
     void* args[] = {&ds, &a, &bar};
     CK(cudaLaunchCooperativeKernel((const void*)ns::stage2_kernel<K>, dim3(s->grid_st2), dim3(s->st2_threads), args,
@@ -390,6 +390,9 @@ ns_status setup_grids(ns_system* s) {
     // split stage loop: CTA size and grid (NS_STAGE2_THREADS / NS_STAGE2_GRID)
     s->st2_threads = 256;  // measured: 64 and 128 are not faster (C3 73.6 / 60.3 vs 62.3 us per stage)
     if (const char* e = getenv("NS_STAGE2_THREADS")) s->st2_threads = std::max(32, std::min(256, atoi(e))) / 32 * 32;
+    // row-owning warps per critical CTA (NS_STAGE2_CW; default all of them)
+    s->st2_cwpb = s->st2_threads / 32;
+    if (const char* e = getenv("NS_STAGE2_CW")) s->st2_cwpb = std::max(1, std::min(s->st2_threads / 32, atoi(e)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, ns::stage2_kernel<K>, s->st2_threads, 0));
     if (occ2 < 1) s->stage_split = false;
     s->grid_st2 = std::min(occ2 * s->sms, s->sms * std::max(1, 256 / s->st2_threads));

@@ -885,6 +885,7 @@ struct Stage2Args {
   int k_lo;            // first active stage (stages below: dx = 0, reading R34); last = s.dc - 1
   long long* tr;       // [d][4] globaltimer stamps of the critical chain (NS_STAGE_TRACE), or nullptr
   double* part;        // [npairs][K][32] per-lane partial sums of the bulk pairs
+  int cwpb;            // warps per critical CTA that own a row (warps 0..cwpb-1; <= blockDim / 32)
 };
 
 __device__ __forceinline__ void sub_sync(unsigned* cnt, unsigned& target, unsigned nq) {
@@ -928,7 +929,9 @@ __global__ void __launch_bounds__(256) stage2_kernel(DevSys s, Stage2Args a, uns
   }
   if ((int)blockIdx.x < a.Q) {
     // ---------------- critical group
-    const int cw = blockIdx.x * wpb + wib, ncw = a.Q * wpb;
+    // warps 0..cwpb-1 own rows (cwpb = 4: one row-owning warp per SMSP, so a row dot
+    // does not share its SMSP's FP64 pipe with another one); the rest only join the barriers
+    const int cw = (wib < a.cwpb) ? blockIdx.x * a.cwpb + wib : n, ncw = a.Q * a.cwpb;
     unsigned target = 0;
     const bool trc = a.tr && blockIdx.x == 0 && threadIdx.x == 0;
     // Each critical warp owns at most one row (ncw >= n).  The stage-invariant

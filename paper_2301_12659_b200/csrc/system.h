@@ -69,6 +69,7 @@ struct ns_system {
   size_t qr_smem_reserve = 0;
   int st_threads = 256;        // threads per CTA of the stage kernel
   int st2_threads = 64, grid_st2 = 0;  // split stage kernel (stage2_kernel): CTA size and grid
+  int st2_cwpb = 2;                    // stage2: row-owning warps per critical CTA
   int qr_threads = 128;        // threads per CTA of the QR kernel
   bool qr_owner_beta = false;  // grid QR: the reflector's owner forms beta (NS_QR_OWNER_BETA)
   bool qr_small_regs = false;  // grid QR: register-light variant, 2 CTAs per SM (n > 128)
